@@ -1,0 +1,157 @@
+/*
+ * pd.h -- C ABI of the B200 (sm_100a) power / Voronoi diagram cell-construction library (libpd.so).
+ *
+ * Problem (§3 Eq. 1): given sites p_i with weights w_i, the power cell
+ *     C_i = { x : |x - p_i|^2 - w_i <= |x - p_j|^2 - w_j  for all j != i }
+ * restricted to the box B (App. "Initialization").  Equal weights give Voronoi.
+ * Two sites are neighbours iff their cells share a polygonal face of positive area.
+ *
+ * Method (the hot path): per cell, progressive half-space clipping of B (§4.1,
+ * App. "Convex cell clipping" PAPER.md:548-558) by the bisecting planes of candidates found by a
+ * best-first traversal (Alg. 1) of a weight-augmented BVH (PAPER.md:295-297,
+ * 526-527) pruned by the directional bound (§4.2).  Output: CSR adjacency,
+ * per-face areas, per-cell volumes and flags (EMPTY etc.) -- SURVEY.md §8(b).
+ *
+ * Conventions (all entry points):
+ *  - No C++ exceptions cross this boundary; every call returns a pd_status.
+ *  - Inputs are BORROWED for the duration of the call and never retained.  They are host pointers
+ *    unless PD_IN_DEVICE is set, in which case they must be device pointers on opt->device.
+ *  - Outputs are OWNED by the pd_result and released by pd_free.  They live on the device unless
+ *    PD_OUT_HOST is set (then they are host memory).  Accessors never transfer ownership.
+ *  - Calls are synchronous with respect to the host: on return the result is complete.  Work is
+ *    enqueued on opt->stream (a cudaStream_t; NULL = the legacy default stream).
+ *  - On error *out is set to NULL and no partial output exists.
+ *  - Thread safety: distinct pd_result objects may be built concurrently from different threads.
+ *  - Ids are int32 (n <= PD_MAX_SITES).  Output is deterministic: byte-identical across runs.
+ */
+#ifndef PD_H
+#define PD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PD_ABI_VERSION 1
+#define PD_MAX_SITES ((int64_t)1 << 26) /* leaf-range encoding of the BVH: 26-bit first index */
+
+typedef struct { float lo[3], hi[3]; } pd_box;
+
+typedef enum {
+    PD_OK = 0,
+    PD_EINVAL = 1,      /* bad argument: n > PD_MAX_SITES, lo >= hi on an axis, NULL where required */
+    PD_EEMPTY = 2,      /* n == 0 */
+    PD_ENONFINITE = 3,  /* a coordinate or weight is NaN/Inf; pd_error_index() names it */
+    PD_EOUTSIDE = 4,    /* a point lies outside the closed box; pd_error_index() names it */
+    PD_ENOMEM = 5,      /* device or host allocation failed */
+    PD_ECUDA = 6,       /* a CUDA runtime error (message via pd_last_cuda_error()) */
+    PD_ENCCL = 7,       /* reserved (collectives live in the Python layer, torch.distributed) */
+    PD_EINTERNAL = 8    /* an internal invariant failed (e.g. output arena overflow twice) */
+} pd_status;
+
+/* pd_options.flags */
+enum {
+    PD_IN_DEVICE = 1u << 0,   /* points/weights are device pointers (else host) */
+    PD_OUT_HOST = 1u << 1,    /* copy the outputs to host memory before returning */
+    PD_STATS = 1u << 2,       /* collect traversal/clipping counters (pd_get_stats) */
+    PD_ISOTROPIC = 1u << 3,   /* ablation: isotropic radius instead of the directional one */
+    PD_DFS = 1u << 4,         /* ablation: depth-first LIFO traversal instead of best-first */
+    PD_AABB_SUPPORT = 1u << 6 /* tighter site test: exact AABB support max_{y in AABB} y.D (not the paper's) */
+};
+
+/* pd_cell_flags values */
+enum {
+    PD_CELL_EMPTY = 1,     /* vol == 0 (power cell empty inside the box) */
+    PD_CELL_BOUNDARY = 2,  /* a box wall contributes a face of positive area */
+    PD_CELL_OVERFLOW = 4,  /* exceeded the largest on-chip capacity tier: output incomplete */
+    PD_CELL_DUPLICATE = 8, /* bit-identical position with a heavier (or equal, lower-id) site */
+    PD_CELL_NOT_OWNED = 32 /* sharded build: this cell belongs to another rank's slice */
+};
+
+typedef struct {
+    int device;        /* CUDA device ordinal */
+    void* stream;      /* cudaStream_t (NULL = default stream) */
+    int leaf_size;     /* BVH leaf size l, 1..32 (0 = default 16); PAPER.md:527 uses 17 / 10 */
+    unsigned flags;    /* PD_* flags above */
+    int shard_rank;    /* sharded build: this rank's slice of the Morton order (0 when world=1) */
+    int shard_world;   /* number of slices (0 or 1 = whole diagram) */
+} pd_options;
+
+typedef struct {
+    int64_t cells;             /* cells built by this call */
+    int64_t nodes_visited;     /* internal BVH nodes whose children were tested (Alg. 1 line 5) */
+    int64_t leaves_visited;    /* leaves processed (Alg. 1 ProcessLeaf) */
+    int64_t sites_tested;      /* leaf sites tested against the directional bound (§4.2) */
+    int64_t clip_tests;        /* candidate planes classified against the cell's vertices */
+    int64_t clips;             /* clips that changed the cell */
+    int64_t tier_cells[3];     /* cells finished in each capacity tier */
+    int64_t overflow_cells;    /* cells flagged PD_CELL_OVERFLOW */
+    int64_t nnz;               /* total neighbour entries */
+    double ms_bvh, ms_cells, ms_csr, ms_total; /* phase times (CUDA events) */
+} pd_stats;
+
+typedef struct pd_result pd_result;
+
+/* Build the diagram of n sites.
+ *  points  : xyz interleaved, 3*n floats (host, or device with PD_IN_DEVICE).
+ *  weights : n floats, or NULL for the Voronoi diagram (all weights 0).
+ *  box     : the domain B (host struct); NULL = the tight AABB of the points.
+ *            Every point must lie in the closed box.
+ *  opt     : options (host struct); NULL = defaults on device 0, default stream.
+ *  out     : receives the result handle (release with pd_free).
+ * Errors: PD_EEMPTY (n == 0), PD_EINVAL, PD_ENONFINITE / PD_EOUTSIDE (index via pd_error_index),
+ *         PD_ENOMEM, PD_ECUDA, PD_EINTERNAL. */
+pd_status pd_build(const float* points, const float* weights, int64_t n, const pd_box* box,
+                   const pd_options* opt, pd_result** out);
+
+/* Accessors (valid until pd_free).  Arrays are in ORIGINAL site order. */
+int64_t pd_num_cells(const pd_result* r);
+int64_t pd_nnz(const pd_result* r);
+int pd_on_host(const pd_result* r);              /* 1 if the arrays below are host memory */
+const int64_t* pd_offsets(const pd_result* r);   /* n+1; offsets[0] = 0, offsets[n] = nnz */
+const int32_t* pd_neighbors(const pd_result* r); /* nnz; per row ascending original ids; never self */
+const float* pd_face_areas(const pd_result* r);  /* nnz; aligned with pd_neighbors */
+const float* pd_volumes(const pd_result* r);     /* n; 0 for EMPTY */
+const float* pd_surface(const pd_result* r);     /* n; total surface area incl. box walls */
+const uint8_t* pd_cell_flags(const pd_result* r);/* n; PD_CELL_* bits */
+pd_status pd_get_stats(const pd_result* r, pd_stats* s);
+void pd_free(pd_result* r);
+
+/* Sharded builds (pd_options.shard_world > 1) compute only this rank's contiguous slice of the
+ * Morton order; the slice's rows are exported in Morton order so that ranks can exchange them and
+ * reassemble the full diagram with pd_assemble (the exchange itself is torch.distributed/NCCL in
+ * the Python layer). */
+int64_t pd_slice_begin(const pd_result* r);      /* first Morton position of this rank's slice */
+int64_t pd_slice_end(const pd_result* r);
+const int32_t* pd_morton_perm(const pd_result* r); /* n; Morton position -> original id (device) */
+
+/* Reassemble a full CSR (original order) from Morton-ordered per-cell blocks gathered from all
+ * ranks.  All pointers are DEVICE pointers on opt->device:
+ *   perm[n] (Morton pos -> original id), cnt[n] (row length per Morton pos), vol/surf/flags[n]
+ *   per Morton pos, rows_nbr/rows_area[total] concatenated rows in Morton order.
+ * Returns a result whose arrays are in original order (on device unless PD_OUT_HOST). */
+pd_status pd_assemble(const int32_t* perm, const int32_t* cnt, const float* vol, const float* surf,
+                      const uint8_t* flags, const int32_t* rows_nbr, const float* rows_area,
+                      int64_t n, int64_t total, const pd_options* opt, pd_result** out);
+
+/* Morton-ordered export of a (sharded) result, for the exchange: copies, for Morton positions
+ * [pd_slice_begin, pd_slice_end), the row lengths, volumes, surfaces, flags and concatenated rows
+ * into caller-provided DEVICE buffers.  Returns the number of row entries written via *total. */
+pd_status pd_export_slice(const pd_result* r, int32_t* cnt, float* vol, float* surf,
+                          uint8_t* flags, int32_t* rows_nbr, float* rows_area, int64_t* total,
+                          void* stream);
+int64_t pd_slice_nnz(const pd_result* r);
+
+const char* pd_strerror(pd_status s);
+int64_t pd_error_index(void);      /* thread-local: offending point of the last NONFINITE/OUTSIDE */
+const char* pd_last_cuda_error(void); /* thread-local message of the last PD_ECUDA */
+int pd_abi_version(void);
+/* Number of kernels launched by the last pd_build/pd_assemble on this thread (for bench.py). */
+int64_t pd_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PD_H */

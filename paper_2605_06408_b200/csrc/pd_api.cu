@@ -1,0 +1,518 @@
+// pd_api.cu -- the C ABI (include/pd.h): argument checking, device memory, the pipeline
+// pack -> Morton -> sort -> gather -> LBVH -> refit -> cell kernel (3 capacity tiers) -> CSR,
+// result ownership and accessors.  See include/pd.h for the contract.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "../../include/pd.h"
+#include "pd_bvh.cuh"
+#include "pd_internal.cuh"
+
+struct pd_result {
+    int64_t n = 0;
+    int64_t nnz = 0;
+    int on_host = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;  // stream the result was built on (frees are ordered on it)
+    int64_t* offsets = nullptr;
+    int32_t* nbr = nullptr;
+    float* area = nullptr;
+    float* vol = nullptr;
+    float* surf = nullptr;
+    uint8_t* flags = nullptr;
+    // sharding
+    int64_t slice_begin = 0, slice_end = 0, slice_nnz = 0;
+    int32_t* perm = nullptr;  // device, Morton position -> original id
+    int32_t* cnt = nullptr;   // device, per original id
+    pd_stats stats;
+    std::vector<void*> dev;
+    std::vector<void*> host;
+};
+
+namespace {
+
+thread_local int64_t g_err_index = -1;
+thread_local char g_cuda_msg[256] = "";
+thread_local int64_t g_launches = 0;
+
+struct Fail {
+    pd_status s;
+};
+
+void ck(cudaError_t e) {
+    if (e != cudaSuccess) {
+        snprintf(g_cuda_msg, sizeof(g_cuda_msg), "%s", cudaGetErrorString(e));
+        if (e == cudaErrorMemoryAllocation) throw Fail{PD_ENOMEM};
+        throw Fail{PD_ECUDA};
+    }
+}
+
+// Stream-ordered allocations, released at scope end (cudaFreeAsync) unless handed to a result.
+struct Arena {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    explicit Arena(cudaStream_t s) : st(s) {}
+    template <class T>
+    T* alloc(size_t count) {
+        void* p = nullptr;
+        size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+        ck(cudaMallocAsync(&p, bytes, st));
+        ptrs.push_back(p);
+        return (T*)p;
+    }
+    void release(void* p) {
+        auto it = std::find(ptrs.begin(), ptrs.end(), p);
+        if (it != ptrs.end()) ptrs.erase(it);
+    }
+    ~Arena() {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+    }
+};
+
+void setup_pool(int device) {
+    static bool done[64] = {false};
+    if (device >= 0 && device < 64 && !done[device]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        done[device] = true;
+    }
+}
+
+int num_sms(int device) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    return v > 0 ? v : 1;
+}
+
+template <class T>
+T* to_result(pd_result* r, Arena& A, T* p) {
+    A.release(p);
+    r->dev.push_back(p);
+    return p;
+}
+
+template <class T>
+T* host_copy(pd_result* r, const T* dptr, size_t count, cudaStream_t st) {
+    T* h = nullptr;
+    ck(cudaMallocHost(&h, std::max<size_t>(count * sizeof(T), 16)));
+    r->host.push_back(h);
+    if (count) ck(cudaMemcpyAsync(h, dptr, count * sizeof(T), cudaMemcpyDeviceToHost, st));
+    return h;
+}
+
+void free_result(pd_result* r) {
+    if (!r) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(r->device);
+    for (void* p : r->dev) cudaFreeAsync(p, r->stream);
+    if (!r->host.empty()) cudaStreamSynchronize(r->stream);
+    for (void* p : r->host) cudaFreeHost(p);
+    cudaSetDevice(cur);
+    delete r;
+}
+
+void finish_outputs(pd_result* r, Arena& A, unsigned flags, cudaStream_t st) {
+    if (flags & PD_OUT_HOST) {
+        r->offsets = host_copy(r, r->offsets, (size_t)r->n + 1, st);
+        r->nbr = host_copy(r, r->nbr, (size_t)r->nnz, st);
+        r->area = host_copy(r, r->area, (size_t)r->nnz, st);
+        r->vol = host_copy(r, r->vol, (size_t)r->n, st);
+        r->surf = host_copy(r, r->surf, (size_t)r->n, st);
+        r->flags = host_copy(r, r->flags, (size_t)r->n, st);
+        r->on_host = 1;
+    }
+    (void)A;
+}
+
+pd_status build_impl(const float* points, const float* weights, int64_t n, const pd_box* box, const pd_options* optp,
+                     pd_result** out) {
+    pd_options opt;
+    memset(&opt, 0, sizeof(opt));
+    if (optp) opt = *optp;
+    if (!out) return PD_EINVAL;
+    *out = nullptr;
+    if (n == 0) return PD_EEMPTY;
+    if (n < 0 || n > PD_MAX_SITES || !points) return PD_EINVAL;
+    if (box)
+        for (int k = 0; k < 3; ++k)
+            if (!(box->lo[k] < box->hi[k]) || !std::isfinite(box->lo[k]) || !std::isfinite(box->hi[k])) return PD_EINVAL;
+    int leaf = opt.leaf_size > 0 ? opt.leaf_size : 16;
+    if (leaf > 32) return PD_EINVAL;
+    int world = opt.shard_world > 1 ? opt.shard_world : 1;
+    int rank = world > 1 ? opt.shard_rank : 0;
+    if (rank < 0 || rank >= world) return PD_EINVAL;
+    g_launches = 0;
+    int launches = 0;
+    ck(cudaSetDevice(opt.device));
+    setup_pool(opt.device);
+    cudaStream_t st = (cudaStream_t)opt.stream;
+    Arena A(st);
+    pd_result* r = new pd_result();
+    memset(&r->stats, 0, sizeof(r->stats));
+    r->n = n;
+    r->device = opt.device;
+    r->stream = (cudaStream_t)opt.stream;
+    try {
+        cudaEvent_t ev[5];
+        for (auto& e : ev) ck(cudaEventCreate(&e));
+        ck(cudaEventRecord(ev[0], st));
+        // ---- inputs
+        const float* dpts = points;
+        const float* dw = weights;
+        if (!(opt.flags & PD_IN_DEVICE)) {
+            float* p = A.alloc<float>((size_t)n * 3);
+            ck(cudaMemcpyAsync(p, points, sizeof(float) * 3 * n, cudaMemcpyHostToDevice, st));
+            dpts = p;
+            if (weights) {
+                float* q = A.alloc<float>((size_t)n);
+                ck(cudaMemcpyAsync(q, weights, sizeof(float) * n, cudaMemcpyHostToDevice, st));
+                dw = q;
+            }
+        }
+        // ---- a1/a2 pack + validate + box
+        float4* sites = A.alloc<float4>(n);
+        float* box_dev = A.alloc<float>(8);
+        unsigned long long* errs = A.alloc<unsigned long long>(2);
+        int* aabb = A.alloc<int>(8);
+        ck(cudaMemsetAsync(errs, 0xff, 2 * sizeof(unsigned long long), st));
+        {
+            int init[6] = {0x7f800000, 0x7f800000, 0x7f800000, (int)(0xff800000u ^ 0x7fffffffu),
+                           (int)(0xff800000u ^ 0x7fffffffu), (int)(0xff800000u ^ 0x7fffffffu)};
+            ck(cudaMemcpyAsync(aabb, init, sizeof(init), cudaMemcpyHostToDevice, st));
+        }
+        if (box) {
+            float b[6] = {box->lo[0], box->lo[1], box->lo[2], box->hi[0], box->hi[1], box->hi[2]};
+            ck(cudaMemcpyAsync(box_dev, b, sizeof(b), cudaMemcpyHostToDevice, st));
+        }
+        ck(pd::bvh_pack(dpts, dw, n, box, sites, box_dev, errs, aabb, st, &launches));
+        unsigned long long herr[2];
+        float hbox[6];
+        ck(cudaMemcpyAsync(herr, errs, sizeof(herr), cudaMemcpyDeviceToHost, st));
+        ck(cudaMemcpyAsync(hbox, box_dev, sizeof(hbox), cudaMemcpyDeviceToHost, st));
+        ck(cudaStreamSynchronize(st));
+        if (herr[0] != ~0ull) { g_err_index = (int64_t)herr[0]; throw Fail{PD_ENONFINITE}; }
+        if (herr[1] != ~0ull) { g_err_index = (int64_t)herr[1]; throw Fail{PD_EOUTSIDE}; }
+        // a degenerate tight box (all points on a plane) is widened so cells stay 3-D
+        if (!box) {
+            bool changed = false;
+            for (int k = 0; k < 3; ++k)
+                if (!(hbox[k] < hbox[3 + k])) {
+                    hbox[k] = std::nextafter(hbox[k], -INFINITY);
+                    hbox[3 + k] = std::nextafter(hbox[3 + k], INFINITY);
+                    changed = true;
+                }
+            if (changed) ck(cudaMemcpyAsync(box_dev, hbox, sizeof(hbox), cudaMemcpyHostToDevice, st));
+        }
+        // ---- a3-a5 Morton, sort, gather
+        uint64_t* keys = A.alloc<uint64_t>(n);
+        uint64_t* keys_s = A.alloc<uint64_t>(n);
+        uint32_t* vals = A.alloc<uint32_t>(n);
+        uint32_t* vals_s = A.alloc<uint32_t>(n);
+        ck(pd::bvh_morton(sites, n, box_dev, keys, vals, st, &launches));
+        size_t tb = 0;
+        ck(pd::sort_pairs(keys, keys_s, vals, vals_s, n, nullptr, &tb, st, nullptr));
+        void* tmp = A.alloc<unsigned char>(tb);
+        ck(pd::sort_pairs(keys, keys_s, vals, vals_s, n, tmp, &tb, st, &launches));
+        float4* sorted = A.alloc<float4>(n);
+        int32_t* perm = A.alloc<int32_t>(n);
+        ck(pd::bvh_gather(sites, vals_s, n, sorted, perm, st, &launches));
+        // ---- a6/a7 LBVH + refit
+        pd::BvhScratch sc;
+        int ni = (int)std::max<int64_t>(n - 1, 1);
+        sc.child = A.alloc<int2>(ni);
+        sc.range = A.alloc<int2>(ni);
+        sc.parent_int = A.alloc<int>(ni);
+        sc.parent_leaf = A.alloc<int>(n);
+        sc.visit = A.alloc<int>(ni);
+        sc.blo = A.alloc<float4>(ni);
+        sc.bhi = A.alloc<float4>(ni);
+        pd::Bvh bvh;
+        bvh.nodes = A.alloc<pd::NodeRec>(ni);
+        bvh.root = A.alloc<pd::NodeChild>(1);
+        bvh.n_internal = (int)(n - 1);
+        ck(pd::bvh_topology(keys_s, sorted, (int)n, leaf, sc, bvh, st, &launches));
+        ck(cudaEventRecord(ev[1], st));
+        // ---- cells
+        int64_t begin = (n * rank) / world, end = (n * (rank + 1)) / world;
+        r->slice_begin = begin;
+        r->slice_end = end;
+        int32_t* cnt = A.alloc<int32_t>(n);
+        int64_t* aoff = A.alloc<int64_t>(n);
+        float* vol = A.alloc<float>(n);
+        float* surf = A.alloc<float>(n);
+        uint8_t* flags = A.alloc<uint8_t>(n);
+        int32_t* lists = A.alloc<int32_t>(2 * (size_t)std::max<int64_t>(end - begin, 1));
+        unsigned long long* counters = A.alloc<unsigned long long>(8);
+        int32_t* list_counts = A.alloc<int32_t>(4);
+        int* aovf = A.alloc<int>(1);
+        pd::Stats* dstats = A.alloc<pd::Stats>(1);
+        int64_t cap = std::max<int64_t>((end - begin) * 18, 1 << 16);
+        int32_t* anbr = nullptr;
+        float* aarea = nullptr;
+        int sms = num_sms(opt.device);
+        for (int attempt = 0; attempt < 3; ++attempt) {
+            anbr = A.alloc<int32_t>(cap);
+            aarea = A.alloc<float>(cap);
+            ck(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), st));
+            ck(cudaMemsetAsync(list_counts, 0, 4 * sizeof(int32_t), st));
+            ck(cudaMemsetAsync(aovf, 0, sizeof(int), st));
+            ck(cudaMemsetAsync(dstats, 0, sizeof(pd::Stats), st));
+            if (world > 1) {
+                ck(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * n, st));
+                ck(pd::fill_flags(flags, n, PD_CELL_NOT_OWNED, st, &launches));
+                ck(cudaMemsetAsync(vol, 0, sizeof(float) * n, st));
+                ck(cudaMemsetAsync(surf, 0, sizeof(float) * n, st));
+            }
+            pd::CellParams P;
+            memset(&P, 0, sizeof(P));
+            P.sites = sorted;
+            P.perm = perm;
+            P.nodes = bvh.nodes;
+            P.root = bvh.root;
+            for (int k = 0; k < 3; ++k) { P.box_lo[k] = hbox[k]; P.box_hi[k] = hbox[3 + k]; }
+            P.flags = opt.flags;
+            P.out.cnt = cnt;
+            P.out.aoff = aoff;
+            P.out.vol = vol;
+            P.out.surf = surf;
+            P.out.flags = flags;
+            P.out.arena_nbr = anbr;
+            P.out.arena_area = aarea;
+            P.out.arena_top = counters + 4;
+            P.out.arena_cap = cap;
+            P.out.arena_overflow = aovf;
+            P.stats = dstats;
+            int64_t L = end - begin;
+            for (int tier = 0; tier < 3; ++tier) {
+                P.work_counter = counters + tier;
+                P.last_tier = tier == 2;
+                if (tier == 0) {
+                    P.begin = begin;
+                    P.count = L;
+                    P.list = nullptr;
+                    P.list_count = nullptr;
+                } else {
+                    P.list = lists + (size_t)((tier - 1) & 1) * std::max<int64_t>(L, 1);
+                    P.list_count = list_counts + (tier - 1);
+                }
+                P.next_list = lists + (size_t)(tier & 1) * std::max<int64_t>(L, 1);
+                P.next_count = list_counts + tier;
+                ck(pd::launch_cells(tier, P, st, sms, &launches));
+            }
+            unsigned long long top = 0;
+            int ovf = 0;
+            ck(cudaMemcpyAsync(&top, counters + 4, sizeof(top), cudaMemcpyDeviceToHost, st));
+            ck(cudaMemcpyAsync(&ovf, aovf, sizeof(ovf), cudaMemcpyDeviceToHost, st));
+            ck(cudaStreamSynchronize(st));
+            if (!ovf) break;
+            if (attempt == 2) throw Fail{PD_EINTERNAL};
+            cap = (int64_t)(top * 1.1) + 1024;  // rerun with an arena large enough
+        }
+        ck(cudaEventRecord(ev[2], st));
+        // ---- a13 CSR
+        int64_t* offsets = A.alloc<int64_t>((size_t)n + 1);
+        size_t sb = 0;
+        ck(pd::scan_counts(cnt, offsets, n, nullptr, &sb, st, nullptr));
+        void* stmp = A.alloc<unsigned char>(sb);
+        ck(pd::scan_counts(cnt, offsets, n, stmp, &sb, st, &launches));
+        int64_t nnz = 0;
+        ck(cudaMemcpyAsync(&nnz, offsets + n, sizeof(nnz), cudaMemcpyDeviceToHost, st));
+        ck(cudaStreamSynchronize(st));
+        int32_t* nbr = A.alloc<int32_t>((size_t)nnz);
+        float* area = A.alloc<float>((size_t)nnz);
+        ck(pd::csr_gather(cnt, aoff, offsets, anbr, aarea, n, nbr, area, st, &launches));
+        ck(cudaEventRecord(ev[3], st));
+        r->nnz = nnz;
+        r->offsets = to_result(r, A, offsets);
+        r->nbr = to_result(r, A, nbr);
+        r->area = to_result(r, A, area);
+        r->vol = to_result(r, A, vol);
+        r->surf = to_result(r, A, surf);
+        r->flags = to_result(r, A, flags);
+        r->perm = to_result(r, A, perm);
+        r->cnt = to_result(r, A, cnt);
+        r->slice_nnz = nnz;
+        finish_outputs(r, A, opt.flags, st);
+        ck(cudaEventRecord(ev[4], st));
+        pd::Stats hs;
+        ck(cudaMemcpyAsync(&hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, st));
+        ck(cudaStreamSynchronize(st));
+        float t01, t12, t23, t04;
+        cudaEventElapsedTime(&t01, ev[0], ev[1]);
+        cudaEventElapsedTime(&t12, ev[1], ev[2]);
+        cudaEventElapsedTime(&t23, ev[2], ev[3]);
+        cudaEventElapsedTime(&t04, ev[0], ev[4]);
+        for (auto& e : ev) cudaEventDestroy(e);
+        pd_stats& s = r->stats;
+        s.cells = (int64_t)hs.cells;
+        s.nodes_visited = (int64_t)hs.nodes;
+        s.leaves_visited = (int64_t)hs.leaves;
+        s.sites_tested = (int64_t)hs.sites;
+        s.clip_tests = (int64_t)hs.clip_tests;
+        s.clips = (int64_t)hs.clips;
+        for (int k = 0; k < 3; ++k) s.tier_cells[k] = (int64_t)hs.tier[k];
+        s.overflow_cells = (int64_t)hs.overflow;
+        s.nnz = nnz;
+        s.ms_bvh = t01;
+        s.ms_cells = t12;
+        s.ms_csr = t23;
+        s.ms_total = t04;
+        g_launches = launches;
+        *out = r;
+        return PD_OK;
+    } catch (const Fail& f) {
+        cudaStreamSynchronize(st);
+        free_result(r);
+        return f.s;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+pd_status pd_build(const float* points, const float* weights, int64_t n, const pd_box* box, const pd_options* opt,
+                   pd_result** out) {
+    try {
+        return build_impl(points, weights, n, box, opt, out);
+    } catch (...) {
+        if (out) *out = nullptr;
+        return PD_EINTERNAL;
+    }
+}
+
+int64_t pd_num_cells(const pd_result* r) { return r ? r->n : 0; }
+int64_t pd_nnz(const pd_result* r) { return r ? r->nnz : 0; }
+int pd_on_host(const pd_result* r) { return r ? r->on_host : 0; }
+const int64_t* pd_offsets(const pd_result* r) { return r ? r->offsets : nullptr; }
+const int32_t* pd_neighbors(const pd_result* r) { return r ? r->nbr : nullptr; }
+const float* pd_face_areas(const pd_result* r) { return r ? r->area : nullptr; }
+const float* pd_volumes(const pd_result* r) { return r ? r->vol : nullptr; }
+const float* pd_surface(const pd_result* r) { return r ? r->surf : nullptr; }
+const uint8_t* pd_cell_flags(const pd_result* r) { return r ? r->flags : nullptr; }
+pd_status pd_get_stats(const pd_result* r, pd_stats* s) {
+    if (!r || !s) return PD_EINVAL;
+    *s = r->stats;
+    return PD_OK;
+}
+void pd_free(pd_result* r) { free_result(r); }
+int64_t pd_slice_begin(const pd_result* r) { return r ? r->slice_begin : 0; }
+int64_t pd_slice_end(const pd_result* r) { return r ? r->slice_end : 0; }
+int64_t pd_slice_nnz(const pd_result* r) { return r ? r->slice_nnz : 0; }
+const int32_t* pd_morton_perm(const pd_result* r) { return r ? r->perm : nullptr; }
+
+pd_status pd_export_slice(const pd_result* r, int32_t* cnt_m, float* vol_m, float* surf_m, uint8_t* flags_m,
+                          int32_t* rows_nbr, float* rows_area, int64_t* total, void* stream) {
+    if (!r || r->on_host || !total) return PD_EINVAL;
+    try {
+        ck(cudaSetDevice(r->device));
+        cudaStream_t st = (cudaStream_t)stream;
+        Arena A(st);
+        int launches = 0;
+        int64_t len = r->slice_end - r->slice_begin;
+        ck(pd::slice_export_meta(r->perm, r->slice_begin, len, r->cnt, r->vol, r->surf, r->flags, cnt_m, vol_m, surf_m,
+                                 flags_m, st, &launches));
+        int64_t* moff = A.alloc<int64_t>((size_t)len + 1);
+        size_t sb = 0;
+        ck(pd::scan_counts(cnt_m, moff, len, nullptr, &sb, st, nullptr));
+        void* tmp = A.alloc<unsigned char>(sb);
+        ck(pd::scan_counts(cnt_m, moff, len, tmp, &sb, st, &launches));
+        ck(pd::slice_export_rows(r->perm, r->slice_begin, len, cnt_m, moff, r->offsets, r->nbr, r->area, rows_nbr,
+                                 rows_area, st, &launches));
+        ck(cudaMemcpyAsync(total, moff + len, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        ck(cudaStreamSynchronize(st));
+        g_launches = launches;
+        return PD_OK;
+    } catch (const Fail& f) {
+        return f.s;
+    }
+}
+
+pd_status pd_assemble(const int32_t* perm, const int32_t* cnt_m, const float* vol_m, const float* surf_m,
+                      const uint8_t* flags_m, const int32_t* rows_nbr, const float* rows_area, int64_t n, int64_t total,
+                      const pd_options* optp, pd_result** out) {
+    pd_options opt;
+    memset(&opt, 0, sizeof(opt));
+    if (optp) opt = *optp;
+    if (!out || n <= 0 || !perm || !cnt_m) return PD_EINVAL;
+    *out = nullptr;
+    pd_result* r = new pd_result();
+    memset(&r->stats, 0, sizeof(r->stats));
+    r->n = n;
+    r->device = opt.device;
+    r->stream = (cudaStream_t)opt.stream;
+    try {
+        ck(cudaSetDevice(opt.device));
+        setup_pool(opt.device);
+        cudaStream_t st = (cudaStream_t)opt.stream;
+        Arena A(st);
+        int launches = 0;
+        int32_t* cnt = A.alloc<int32_t>(n);
+        float* vol = A.alloc<float>(n);
+        float* surf = A.alloc<float>(n);
+        uint8_t* flags = A.alloc<uint8_t>(n);
+        ck(pd::assemble_meta(perm, n, cnt_m, vol_m, surf_m, flags_m, cnt, vol, surf, flags, st, &launches));
+        int64_t* moff = A.alloc<int64_t>((size_t)n + 1);
+        int64_t* offsets = A.alloc<int64_t>((size_t)n + 1);
+        size_t sb = 0;
+        ck(pd::scan_counts(cnt_m, moff, n, nullptr, &sb, st, nullptr));
+        void* tmp = A.alloc<unsigned char>(sb);
+        ck(pd::scan_counts(cnt_m, moff, n, tmp, &sb, st, &launches));
+        size_t sb2 = 0;
+        ck(pd::scan_counts(cnt, offsets, n, nullptr, &sb2, st, nullptr));
+        void* tmp2 = A.alloc<unsigned char>(sb2);
+        ck(pd::scan_counts(cnt, offsets, n, tmp2, &sb2, st, &launches));
+        int32_t* nbr = A.alloc<int32_t>((size_t)total);
+        float* area = A.alloc<float>((size_t)total);
+        ck(pd::assemble_rows(perm, n, cnt_m, moff, offsets, rows_nbr, rows_area, nbr, area, st, &launches));
+        r->nnz = total;
+        r->offsets = to_result(r, A, offsets);
+        r->nbr = to_result(r, A, nbr);
+        r->area = to_result(r, A, area);
+        r->vol = to_result(r, A, vol);
+        r->surf = to_result(r, A, surf);
+        r->flags = to_result(r, A, flags);
+        r->cnt = to_result(r, A, cnt);
+        r->slice_begin = 0;
+        r->slice_end = n;
+        finish_outputs(r, A, opt.flags, st);
+        ck(cudaStreamSynchronize(st));
+        g_launches = launches;
+        *out = r;
+        return PD_OK;
+    } catch (const Fail& f) {
+        free_result(r);
+        return f.s;
+    }
+}
+
+const char* pd_strerror(pd_status s) {
+    switch (s) {
+        case PD_OK: return "ok";
+        case PD_EINVAL: return "invalid argument";
+        case PD_EEMPTY: return "empty input (n == 0)";
+        case PD_ENONFINITE: return "non-finite coordinate or weight";
+        case PD_EOUTSIDE: return "point outside the box";
+        case PD_ENOMEM: return "out of memory";
+        case PD_ECUDA: return "CUDA error";
+        case PD_ENCCL: return "NCCL error";
+        case PD_EINTERNAL: return "internal error";
+    }
+    return "unknown status";
+}
+int64_t pd_error_index(void) { return g_err_index; }
+const char* pd_last_cuda_error(void) { return g_cuda_msg; }
+int pd_abi_version(void) { return PD_ABI_VERSION; }
+int64_t pd_last_launch_count(void) { return g_launches; }
+
+}  // extern "C"

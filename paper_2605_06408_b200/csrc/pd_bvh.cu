@@ -1,0 +1,260 @@
+// pd_bvh.cu -- input packing, Morton codes, radix sort, Karras LBVH topology and
+// the bottom-up refit of per-node AABB + max weight ("power-augmented BVH").
+// The paper uses the cuBQL builder; this is an own LBVH (Karras 2012 topology over 63-bit Morton
+// codes), collapsed to leaves of <= l sites at traversal time via the leaf-range links.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pd_bvh.cuh"
+#include "pd_internal.cuh"
+
+namespace pd {
+namespace {
+
+__device__ __forceinline__ int ford(float f) {
+    int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float iford(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+// a1: pack (x,y,z,w) into one float4 per site; validate finite and (if a box is given) inside it.
+__global__ void k_pack(const float* __restrict__ pts, const float* __restrict__ w, int64_t n, float4* __restrict__ out,
+                       int has_box, float lx, float ly, float lz, float hx, float hy, float hz,
+                       unsigned long long* err_nonfinite, unsigned long long* err_outside, int* aabb) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    if (i < n) {
+        float x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+        float ww = w ? w[i] : 0.f;
+        out[i] = make_float4(x, y, z, ww);
+        bool fin = isfinite(x) && isfinite(y) && isfinite(z) && isfinite(ww);
+        if (!fin) atomicMin(err_nonfinite, (unsigned long long)i);
+        else if (has_box && !(x >= lx && x <= hx && y >= ly && y <= hy && z >= lz && z <= hz))
+            atomicMin(err_outside, (unsigned long long)i);
+        if (fin) { mn[0] = mx[0] = x; mn[1] = mx[1] = y; mn[2] = mx[2] = z; }
+    }
+    if (!has_box) {  // a2: AABB of the points
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            int a = __reduce_min_sync(0xffffffffu, ford(mn[k]));
+            int b = __reduce_max_sync(0xffffffffu, ford(mx[k]));
+            if ((threadIdx.x & 31) == 0) {
+                atomicMin(&aabb[k], a);
+                atomicMax(&aabb[3 + k], b);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ uint64_t spread21(uint32_t v) {
+    uint64_t x = v & 0x1fffff;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+// a3: 63-bit Morton code, 21 bits per axis over the box.
+__global__ void k_morton(const float4* __restrict__ s, int64_t n, const float* __restrict__ box, uint64_t* __restrict__ keys,
+                         uint32_t* __restrict__ vals) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float4 p = s[i];
+    float c[3] = {p.x, p.y, p.z};
+    uint32_t q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float ext = box[3 + k] - box[k];
+        float t = ext > 0.f ? (c[k] - box[k]) / ext : 0.f;
+        t = fminf(fmaxf(t, 0.f), 1.f);
+        uint32_t v = (uint32_t)(t * 2097152.0f);
+        q[k] = v > 2097151u ? 2097151u : v;
+    }
+    keys[i] = spread21(q[0]) | (spread21(q[1]) << 1) | (spread21(q[2]) << 2);
+    vals[i] = (uint32_t)i;
+}
+
+// a5: sites in Morton order
+__global__ void k_gather(const float4* __restrict__ s, const uint32_t* __restrict__ perm, int64_t n, float4* __restrict__ out,
+                         int32_t* __restrict__ perm_i32) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t p = perm[i];
+    out[i] = s[p];
+    perm_i32[i] = (int32_t)p;
+}
+
+__device__ __forceinline__ int delta(const uint64_t* __restrict__ k, int n, int i, int j) {
+    if (j < 0 || j >= n) return -1;
+    uint64_t a = k[i], b = k[j];
+    if (a == b) return 64 + __clz((unsigned)(i ^ j));
+    return __clzll((long long)(a ^ b));
+}
+
+// a6: Karras (2012) radix-tree topology.  child >= 0 internal index, child < 0 leaf ~prim.
+__global__ void k_karras(const uint64_t* __restrict__ k, int n, int2* __restrict__ child, int2* __restrict__ range,
+                         int* __restrict__ parent_int, int* __restrict__ parent_leaf) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
+    int dmin = delta(k, n, i, i - d);
+    int lmax = 2;
+    while (delta(k, n, i, i + lmax * d) > dmin) lmax <<= 1;
+    int l = 0;
+    for (int t = lmax >> 1; t >= 1; t >>= 1)
+        if (delta(k, n, i, i + (l + t) * d) > dmin) l += t;
+    int j = i + l * d;
+    int dnode = delta(k, n, i, j);
+    int s = 0;
+    int t = l;
+    do {
+        t = (t + 1) >> 1;
+        if (delta(k, n, i, i + (s + t) * d) > dnode) s += t;
+    } while (t > 1);
+    int gamma = i + s * d + (d < 0 ? d : 0);
+    int lo = min(i, j), hi = max(i, j);
+    int left = (lo == gamma) ? ~gamma : gamma;
+    int right = (hi == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+    child[i] = make_int2(left, right);
+    range[i] = make_int2(lo, hi);
+    if (left < 0) parent_leaf[~left] = i; else parent_int[left] = i;
+    if (right < 0) parent_leaf[~right] = i; else parent_int[right] = i;
+    if (i == 0) parent_int[0] = -1;
+}
+
+// a7: bottom-up refit of AABB + max weight (atomic visit counters; second arrival computes).
+__global__ void k_refit(const float4* __restrict__ s, int n, const int2* __restrict__ child, const int* __restrict__ parent_int,
+                        const int* __restrict__ parent_leaf, int* __restrict__ visit, float4* __restrict__ blo,
+                        float4* __restrict__ bhi) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    int node = parent_leaf[p];
+    while (node >= 0) {
+        __threadfence();
+        if (atomicAdd(&visit[node], 1) == 0) return;
+        __threadfence();
+        int2 c = child[node];
+        float4 lo = make_float4(INFINITY, INFINITY, INFINITY, -INFINITY);
+        float4 hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            int ch = q ? c.y : c.x;
+            float4 a, b;
+            if (ch < 0) {
+                a = s[~ch];
+                b = a;
+            } else {
+                a = __ldcg(&blo[ch]);
+                b = __ldcg(&bhi[ch]);
+            }
+            lo.x = fminf(lo.x, a.x); lo.y = fminf(lo.y, a.y); lo.z = fminf(lo.z, a.z); lo.w = fmaxf(lo.w, a.w);
+            hi.x = fmaxf(hi.x, b.x); hi.y = fmaxf(hi.y, b.y); hi.z = fmaxf(hi.z, b.z);
+        }
+        __stcg(&blo[node], lo);
+        __stcg(&bhi[node], hi);
+        node = parent_int[node];
+    }
+}
+
+// Pack the child records each internal node stores for its two children; children with <= l
+// sites become leaf-range links (the collapse of PAPER.md:527's leaf size l).
+__global__ void k_records(const float4* __restrict__ s, int n, int leaf, const int2* __restrict__ child,
+                          const int2* __restrict__ range, const float4* __restrict__ blo, const float4* __restrict__ bhi,
+                          NodeRec* __restrict__ rec, NodeChild* __restrict__ root) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    int2 c = child[i];
+    int2 r = range[i];
+    int gamma = c.x < 0 ? ~c.x : range[c.x].y;  // left child covers [r.x, gamma]
+    NodeRec out;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        int ch = q ? c.y : c.x;
+        int first = q ? gamma + 1 : r.x;
+        int last = q ? r.y : gamma;
+        int cnt = last - first + 1;
+        float4 a, b;
+        int link;
+        if (ch < 0) {
+            a = s[~ch];
+            b = a;
+            link = leaf_link(~ch, 1);
+        } else {
+            a = blo[ch];
+            b = bhi[ch];
+            link = cnt <= leaf ? leaf_link(first, cnt) : ch;
+        }
+        out.c[q].lo_w = a;
+        out.c[q].hi_l = make_float4(b.x, b.y, b.z, __int_as_float(link));
+    }
+    rec[i] = out;
+    if (i == 0) {
+        float4 lo = make_float4(fminf(out.c[0].lo_w.x, out.c[1].lo_w.x), fminf(out.c[0].lo_w.y, out.c[1].lo_w.y),
+                                fminf(out.c[0].lo_w.z, out.c[1].lo_w.z), fmaxf(out.c[0].lo_w.w, out.c[1].lo_w.w));
+        int rl = n <= leaf ? leaf_link(0, n) : 0;
+        root->lo_w = lo;
+        root->hi_l = make_float4(fmaxf(out.c[0].hi_l.x, out.c[1].hi_l.x), fmaxf(out.c[0].hi_l.y, out.c[1].hi_l.y),
+                                 fmaxf(out.c[0].hi_l.z, out.c[1].hi_l.z), __int_as_float(rl));
+    }
+}
+
+__global__ void k_root_single(NodeChild* root) {
+    root->lo_w = make_float4(0, 0, 0, 0);
+    root->hi_l = make_float4(0, 0, 0, __int_as_float(leaf_link(0, 1)));
+}
+
+__global__ void k_box_from_aabb(const int* aabb, float* box) {
+    int k = threadIdx.x;
+    if (k < 6) box[k] = iford(aabb[k]);
+}
+
+inline unsigned blocks(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+}  // namespace
+
+cudaError_t bvh_pack(const float* pts, const float* w, int64_t n, const pd_box* box, float4* sites, float* box_dev,
+                     unsigned long long* errs, int* aabb, cudaStream_t st, int* launches) {
+    if (box) {
+        k_pack<<<blocks(n, 256), 256, 0, st>>>(pts, w, n, sites, 1, box->lo[0], box->lo[1], box->lo[2], box->hi[0],
+                                               box->hi[1], box->hi[2], errs, errs + 1, aabb);
+        ++*launches;
+    } else {
+        k_pack<<<blocks(n, 256), 256, 0, st>>>(pts, w, n, sites, 0, 0, 0, 0, 0, 0, 0, errs, errs + 1, aabb);
+        k_box_from_aabb<<<1, 32, 0, st>>>(aabb, box_dev);
+        *launches += 2;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t bvh_morton(const float4* sites, int64_t n, const float* box_dev, uint64_t* keys, uint32_t* vals,
+                       cudaStream_t st, int* launches) {
+    k_morton<<<blocks(n, 256), 256, 0, st>>>(sites, n, box_dev, keys, vals);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t bvh_gather(const float4* sites, const uint32_t* perm, int64_t n, float4* sorted, int32_t* perm_i32,
+                       cudaStream_t st, int* launches) {
+    k_gather<<<blocks(n, 256), 256, 0, st>>>(sites, perm, n, sorted, perm_i32);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t bvh_topology(const uint64_t* keys_sorted, const float4* sorted, int n, int leaf, BvhScratch& sc, Bvh& out,
+                         cudaStream_t st, int* launches) {
+    if (n <= 1) {
+        k_root_single<<<1, 1, 0, st>>>(out.root);
+        ++*launches;
+        return cudaGetLastError();
+    }
+    k_karras<<<blocks(n - 1, 256), 256, 0, st>>>(keys_sorted, n, sc.child, sc.range, sc.parent_int, sc.parent_leaf);
+    cudaMemsetAsync(sc.visit, 0, sizeof(int) * (size_t)(n - 1), st);
+    k_refit<<<blocks(n, 256), 256, 0, st>>>(sorted, n, sc.child, sc.parent_int, sc.parent_leaf, sc.visit, sc.blo, sc.bhi);
+    k_records<<<blocks(n - 1, 256), 256, 0, st>>>(sorted, n, leaf, sc.child, sc.range, sc.blo, sc.bhi, out.nodes, out.root);
+    *launches += 3;
+    return cudaGetLastError();
+}
+
+}  // namespace pd

@@ -1,0 +1,73 @@
+// pd_internal.cuh -- shared device types of the CUDA path (never included by oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pd.h"
+
+namespace pd {
+
+// Child record stored in its parent so that the two children of a node are one 64-byte read.
+//   lo_w = (lo.x, lo.y, lo.z, max weight in subtree)   -- PAPER.md:527 "maxweight"
+//   hi_l = (hi.x, hi.y, hi.z, link as int bits)
+// link >= 0 : internal node index; link < 0 : leaf range, ~link = (first << 5) | (count - 1).
+struct __align__(16) NodeChild {
+    float4 lo_w;
+    float4 hi_l;
+};
+struct __align__(64) NodeRec {
+    NodeChild c[2];
+};
+
+__host__ __device__ inline int leaf_link(int first, int count) { return ~((first << 5) | (count - 1)); }
+__host__ __device__ inline int leaf_first(int link) { return (~link) >> 5; }
+__host__ __device__ inline int leaf_count(int link) { return ((~link) & 31) + 1; }
+
+struct Bvh {
+    NodeRec* nodes = nullptr;   // n-1 internal nodes (Karras order); unused when n <= leaf
+    NodeChild* root = nullptr;  // device: 1 record describing the root (bounds + link)
+    int n_internal = 0;
+};
+
+// Per-cell outputs of the cell kernel, indexed by ORIGINAL id (cells outside a shard untouched).
+struct CellOut {
+    int32_t* cnt;        // neighbour count
+    int64_t* aoff;       // offset of the row in the arena
+    float* vol;
+    float* surf;
+    uint8_t* flags;
+    int32_t* arena_nbr;
+    float* arena_area;
+    unsigned long long* arena_top;  // atomic bump pointer (entries)
+    int64_t arena_cap;
+    int* arena_overflow;            // set to 1 when a row did not fit
+};
+
+struct Stats {  // device counters (PD_STATS)
+    unsigned long long nodes, leaves, sites, clip_tests, clips, cells, tier[3], overflow;
+};
+
+struct CellParams {
+    const float4* sites;  // Morton-sorted (x, y, z, w)
+    const int32_t* perm;  // Morton position -> original id
+    const NodeRec* nodes;
+    const NodeChild* root;
+    float box_lo[3], box_hi[3];
+    unsigned flags;
+    // work: either the Morton range [begin, begin+count) or list[0..*list_count)
+    int64_t begin;
+    int64_t count;
+    const int32_t* list;
+    const int32_t* list_count;
+    unsigned long long* work_counter;
+    // overflow hand-off to the next tier
+    int32_t* next_list;
+    int32_t* next_count;
+    int last_tier;
+    CellOut out;
+    Stats* stats;
+};
+
+cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches);
+
+}  // namespace pd

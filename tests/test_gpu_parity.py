@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the same seeded inputs.
+
+Full diagrams at oracle-friendly sizes that span many warps/leaves and a ragged tail; sampled cells
+(random + degree tail + BOUNDARY + EMPTY + OVERFLOW strata) at BASELINE.json's full sizes in the
+launch configuration bench.py times; plus properties that hold at any size (symmetry, partition of
+the box), determinism, ablation neutrality, sharded reassembly and the error contract.
+"""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import pdgen  # noqa: E402
+import paper_2605_06408_b200 as pd  # noqa: E402
+from compare import compare, sample_cells  # noqa: E402
+
+NT = os.cpu_count() or 8
+
+
+def _gpu(wl, **kw):
+    p = torch.from_numpy(wl.points).cuda()
+    w = None if wl.weights is None else torch.from_numpy(wl.weights).cuda()
+    d = pd.build_diagram(p, w, wl.box, **kw)
+    torch.cuda.synchronize()
+    return d.to_numpy()
+
+
+def _assert_parity(wl, ids=None, **kw):
+    g = _gpu(wl, **kw)
+    o = oracle.cells(wl.points, wl.weights, wl.box, ids=ids, threads=NT)
+    rep = compare(g, o)
+    print(wl.name, wl.n, rep.summary())
+    assert rep.ok, rep.summary()
+    return g, o, rep
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    pd.load_library()
+
+
+# ----------------------------------------------------------------- full diagrams, small sizes
+
+def test_c1_full():
+    _assert_parity(pdgen.make("C1"))
+
+
+@pytest.mark.parametrize("cfg,n", [("C2", 20011), ("C3", 20011), ("C4", 20011), ("C5", 20011)])
+def test_configs_full_small(cfg, n):
+    _assert_parity(pdgen.make(cfg, n=n))
+
+
+@pytest.mark.parametrize("leaf", [1, 7, 16, 32])
+def test_leaf_sizes_identical(leaf):
+    wl = pdgen.make("C5", n=5003)
+    ref = _gpu(wl)
+    g = _gpu(wl, leaf_size=leaf)
+    assert np.array_equal(ref.offsets, g.offsets) and np.array_equal(ref.neighbors, g.neighbors)
+    assert np.allclose(ref.volumes, g.volumes, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("flag", [pd.ISOTROPIC, pd.DFS, pd.AABB_SUPPORT])
+def test_ablations_neutral(flag):
+    """Culling / traversal variants change the work, not the diagram."""
+    wl = pdgen.make("C3", n=8009)
+    ref = _gpu(wl)
+    g = _gpu(wl, flags=flag)
+    assert np.array_equal(ref.offsets, g.offsets) and np.array_equal(ref.neighbors, g.neighbors)
+    assert np.allclose(ref.volumes, g.volumes, rtol=1e-6)
+
+
+def test_determinism_bitwise():
+    wl = pdgen.make("C4", n=30011)
+    a, b = _gpu(wl), _gpu(wl)
+    for k in ("offsets", "neighbors", "areas", "volumes", "surface", "flags"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_host_and_device_inputs_identical():
+    wl = pdgen.make("C3", n=7001)
+    a = _gpu(wl)
+    b = pd.build_diagram(wl.points, wl.weights, wl.box, out_host=True)
+    for k in ("offsets", "neighbors", "areas", "volumes", "flags"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+# ----------------------------------------------------------------- special / degenerate inputs
+
+def test_lattice_and_separable_grid():
+    import brute
+    X, Y, Z = [0, 2, 3, 7, 8, 11], [1, 4, 5, 9], [0, 3, 4, 6, 10]
+    f, g, h = [0, 1, -3, 2, 0, 1], [0, -1, 2, 0], [1, 0, 0, -2, 0]
+    box = (-1, -1, -2, 12, 11, 11)
+    pts, wts, vols, nbrs = brute.separable_grid_cells(X, Y, Z, f, g, h, box)
+    d = pd.build_diagram(pts, wts, box, out_host=True)
+    for t in range(len(pts)):
+        assert d.volumes[t] == pytest.approx(float(vols[t]), rel=1e-6, abs=1e-6)
+        nb, ar = d.row(t)
+        assert list(nb) == sorted(nbrs[t].keys())
+    # cubic lattices (cospherical: zero-area contacts must not become neighbours)
+    for kind, vol, deg in (("sc", 1.0, 6), ("bcc", 0.5, 14), ("fcc", 0.25, 12)):
+        gr = np.arange(-3, 4, dtype=np.float64)
+        base = np.stack(np.meshgrid(gr, gr, gr, indexing="ij"), -1).reshape(-1, 3)
+        if kind == "sc":
+            P = base
+        elif kind == "bcc":
+            P = np.concatenate([base, base + 0.5])
+        else:
+            P = np.concatenate([base, base + [0.5, 0.5, 0], base + [0.5, 0, 0.5], base + [0, 0.5, 0.5]])
+        P = (P * 0.5).astype(np.float32)
+        dd = pd.build_diagram(P, None, (-1.8,) * 3 + (1.8,) * 3, out_host=True)
+        c = int(np.argmin(np.sum(P.astype(np.float64) ** 2, axis=1)))
+        nb, ar = dd.row(c)
+        big = ar > 1e-9 * dd.surface[c]
+        assert big.sum() == deg, kind
+        assert dd.volumes[c] == pytest.approx(vol * 0.125, rel=1e-6)
+
+
+def test_tiny_and_degenerate_inputs():
+    box = (0, 0, 0, 1, 1, 1)
+    d = pd.build_diagram(np.array([[0.5, 0.5, 0.5]], np.float32), None, box, out_host=True)
+    assert d.nnz == 0 and d.volumes[0] == pytest.approx(1.0) and d.flags[0] & pd.CELL_BOUNDARY
+    d = pd.build_diagram(np.array([[0.25, 0.5, 0.5], [0.75, 0.5, 0.5]], np.float32), None, box, out_host=True)
+    assert list(d.neighbors) == [1, 0] and np.allclose(d.volumes, 0.5)
+    # duplicates: the heavier owns, ties to the lower id
+    pts = np.array([[0.5, 0.5, 0.5], [0.25, 0.5, 0.5], [0.5, 0.5, 0.5], [0.75, 0.5, 0.5]], np.float32)
+    d = pd.build_diagram(pts, None, box, out_host=True)
+    assert d.flags[2] & pd.CELL_DUPLICATE and d.flags[2] & pd.CELL_EMPTY and not d.flags[0] & pd.CELL_EMPTY
+    # sites on the box boundary, points on a plane with the tight AABB (box=None)
+    pts = pdgen.white_noise(500, 9, 0.0, 1.0)
+    pts[:50, 0] = 0.0
+    pts[50:100, 2] = 1.0
+    _assert_parity(pdgen.Workload("edge", pts, None, box, ""))
+    flat = pts.copy()
+    flat[:, 2] = 0.5
+    g = pd.build_diagram(flat, None, None, out_host=True)
+    assert np.isfinite(g.volumes).all()
+    # a weight so large that other cells become EMPTY
+    pts = pdgen.white_noise(300, 5, 0.0, 1.0)
+    w = np.zeros(300, np.float32)
+    w[7] = 0.2
+    _assert_parity(pdgen.Workload("heavy", pts, w, box, ""))
+
+
+def test_error_contract():
+    box = (0, 0, 0, 1, 1, 1)
+    pts = pdgen.white_noise(100, 3, 0.0, 1.0)
+    bad = pts.copy()
+    bad[42, 1] = np.nan
+    with pytest.raises(pd.PdError) as e:
+        pd.build_diagram(bad, None, box)
+    assert e.value.status == pd.PD_ENONFINITE and e.value.index == 42
+    bad = pts.copy()
+    bad[17, 0] = 1.5
+    with pytest.raises(pd.PdError) as e:
+        pd.build_diagram(bad, None, box)
+    assert e.value.status == pd.PD_EOUTSIDE and e.value.index == 17
+    with pytest.raises(pd.PdError) as e:
+        pd.build_diagram(np.zeros((0, 3), np.float32), None, box)
+    assert e.value.status == pd.PD_EEMPTY
+
+
+def test_sharded_reassembly_matches_single():
+    """world=k slices exported in Morton order and reassembled == the world=1 diagram, bytewise."""
+    wl = pdgen.make("C5", n=40009)
+    ref = _gpu(wl)
+    p = torch.from_numpy(wl.points).cuda()
+    w = torch.from_numpy(wl.weights).cuda()
+    for world in (2, 3):
+        parts = []
+        perm = None
+        for r in range(world):
+            d = pd.build_diagram(p, w, wl.box, shard_rank=r, shard_world=world)
+            parts.append(pd.export_slice(d))
+            if perm is None:
+                perm = pd.morton_perm(d).clone()
+        cat = [torch.cat([pp[k] for pp in parts]) for k in range(6)]
+        full = pd.assemble(perm, *cat).to_numpy()
+        for k in ("offsets", "neighbors", "areas", "volumes", "surface", "flags"):
+            assert np.array_equal(getattr(ref, k), getattr(full, k)), (world, k)
+
+
+# ----------------------------------------------------------------- full sizes, sampled cells
+
+FULL = [("C2", 256), ("C3", 128), ("C4", 96), ("C5", 64)]
+
+
+@pytest.mark.parametrize("cfg,nrand", FULL)
+def test_full_size_sampled(cfg, nrand):
+    wl = pdgen.make(cfg)
+    g = _gpu(wl)
+    ids = sample_cells(g, wl.n, seed=123, n_random=nrand, n_stratum=max(8, nrand // 8))
+    o = oracle.cells(wl.points, wl.weights, wl.box, ids=ids, threads=NT)
+    rep = compare(g, o)
+    print(cfg, rep.summary())
+    assert rep.ok, rep.summary()
+    # properties over ALL cells: box partition and adjacency symmetry
+    bx = np.asarray(wl.box, np.float64)
+    assert g.volumes.astype(np.float64).sum() == pytest.approx(np.prod(bx[3:] - bx[:3]), rel=1e-5)
+    rows = np.repeat(np.arange(wl.n), np.diff(g.offsets))
+    fwd = rows.astype(np.int64) * wl.n + g.neighbors
+    bwd = g.neighbors.astype(np.int64) * wl.n + rows
+    assert np.array_equal(np.sort(fwd), np.sort(bwd))
+    assert not np.any(g.flags & pd.CELL_OVERFLOW)
