@@ -1,0 +1,304 @@
+#!/usr/bin/env python3
+"""bench.py -- Mcells/s of the B200 power-diagram path on BASELINE.json's headline workload.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+A "step" is one full pd_build (pack, Morton, sort, LBVH, refit, cell kernel, CSR) over the whole
+synthetic workload, inputs resident in HBM (value), and the same through the C ABI with pinned host
+buffers + host outputs (e2e).  At N=1 the workload is C4 (10M scene-like power diagram,
+BASELINE.json configs[3], the config the metric is quoted on).  For N>1 (torchrun, one rank per GPU)
+the cells are split into Morton slices (strong scaling: the 10M diagram is fixed), exchanged with
+NCCL all-gathers and reassembled on every rank; time = max over ranks.
+
+`--impl reference` times the CPU oracle (oracle/, the reference arm of this tier) on host cores on a
+bounded sample of the same workload's cells per step; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "Mcells/s for 10M-point power diagram"
+UNIT = "Mcells/s"
+# Algorithmic FP work per cell (SURVEY.md §8(d) "Algorithmic work per cell": W_min ≈ 25·300 node
+# tests + 15·450 site tests + 4·27·77 vertex classifications + 40·27 vertex creations ≈ 2.3e4
+# FP ops/cell).  Peak = 148 SMs × 128 FP32 lanes × 1.965 GHz (B200_PROFILING.md nominal units).
+W_MIN_OPS_PER_CELL = 2.3e4
+ALU_PEAK_TOPS = 148 * 128 * 1.965e9 / 1e12
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_workload(cfg: str, n: int | None):
+    import pdgen
+    t = time.time()
+    wl = pdgen.make(cfg, n=n)
+    return wl, time.time() - t
+
+
+def cpu_baseline(wl, budget_s: float = 15.0, seed: int = 7):
+    """The oracle as it stands, on host cores, on a bounded random sample of the workload's cells."""
+    import oracle
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(seed)
+    probe = rng.choice(wl.n, size=min(wl.n, 2 * threads), replace=False)
+    t = time.time()
+    oracle.cells(wl.points, wl.weights, wl.box, ids=probe, threads=threads)
+    dt = max(time.time() - t, 1e-6)
+    m = int(min(wl.n, max(len(probe), len(probe) * budget_s / dt)))
+    ids = rng.choice(wl.n, size=m, replace=False)
+    t = time.time()
+    oracle.cells(wl.points, wl.weights, wl.box, ids=ids, threads=threads)
+    dt = time.time() - t
+    return {"value": m / dt / 1e6, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{m} random cells of {wl.name} ({wl.n} sites), full brute-force clip per cell, "
+                      f"{dt:.1f} s wall on {threads} threads"}
+
+
+def profile_traffic():
+    """DRAM bytes per launch of the cell kernel from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "cells_kernel_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+def run_reference(args):
+    rank, world, _ = _env_rank()
+    if world > 1 and rank != 0:
+        return 0
+    import oracle
+    wl, _ = load_workload(args.config, args.n)
+    threads = os.cpu_count() or 1
+    per_step = max(threads, args.ref_cells)
+    rng = np.random.default_rng(11)
+    times = []
+    for it in range(args.warmup + args.steps):
+        ids = rng.choice(wl.n, size=per_step, replace=False)
+        t = time.time()
+        oracle.cells(wl.points, wl.weights, wl.box, ids=ids, threads=threads)
+        dt = time.time() - t
+        if it >= args.warmup:
+            times.append(dt)
+    ms = 1e3 * float(np.mean(times))
+    value = per_step / (ms / 1e3) / 1e6
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{wl.name}: {wl.description}", "n": wl.n,
+                       "sample_per_step": per_step},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{per_step} random cells of {wl.name} per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2605_06408_b200 as pd
+    from paper_2605_06408_b200 import build as pdbuild
+    from paper_2605_06408_b200 import dist as pddist
+
+    rank, world, local = _env_rank()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    if rank == 0:
+        pdbuild.build()
+    if world > 1:
+        dist.barrier()
+    pd.load_library()
+    wl, gen_s = load_workload(args.config, args.n)
+    dev = torch.device("cuda", local)
+    p = torch.from_numpy(wl.points).to(dev)
+    w = None if wl.weights is None else torch.from_numpy(wl.weights).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step(flags=0):
+        if world > 1:
+            return pddist.build_diagram_distributed(p, w, wl.box, leaf_size=args.leaf, flags=flags)
+        return pd.build_diagram(p, w, wl.box, leaf_size=args.leaf, flags=flags)
+
+    for _ in range(args.warmup):
+        d = step()
+        del d
+    torch.cuda.synchronize()
+    # stats pass (counters), not timed
+    d = pd.build_diagram(p, w, wl.box, leaf_size=args.leaf, flags=pd.STATS, shard_rank=rank, shard_world=world)
+    stats = dict(d.stats)
+    nnz_total = int(d.nnz)
+    flags_np = d.flags.cpu().numpy()
+    del d
+    sampler = ClockSampler(local)
+    sampler.start()
+    step_ms, cell_ms, launches = [], [], 0
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        d = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        launches += pd.last_launch_count()
+        step_ms.append(e0.elapsed_time(e1))
+        if world == 1:
+            cell_ms.append(d.stats["ms_cells"])
+        del d
+    clocks = sampler.stop()
+    ms = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = wl.n / (ms / 1e3) / 1e6
+
+    # ---- e2e through the C ABI with pinned host buffers and host outputs
+    hp = torch.from_numpy(wl.points).pin_memory()
+    hw = None if wl.weights is None else torch.from_numpy(wl.weights).pin_memory()
+    e2e_ms = []
+    h2d = hp.numel() * 4 + (0 if hw is None else hw.numel() * 4)
+    d2h = 0
+    for it in range(1 + args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pts = hp.numpy()
+        d = pd.build_diagram(pts, None if hw is None else hw.numpy(), wl.box, leaf_size=args.leaf, out_host=True,
+                             shard_rank=rank, shard_world=world)
+        dt = time.perf_counter() - t0
+        d2h = (d.n + 1) * 8 + d.nnz * 8 + d.n * 9
+        del d
+        if it > 0:
+            e2e_ms.append(dt * 1e3)
+    e2e_v = wl.n / (float(np.mean(e2e_ms)) / 1e3) / 1e6
+    if world > 1:
+        t = torch.tensor([e2e_v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        e2e_v = float(t.item())
+
+    line = None
+    if rank == 0:
+        cells_rank = stats["cells"]
+        kms = float(np.mean(cell_ms)) if cell_ms else stats["ms_cells"]
+        achieved = W_MIN_OPS_PER_CELL * cells_rank / (kms / 1e3) / 1e12
+        traffic = profile_traffic()
+        roof = {"bound": "alu", "achieved": achieved, "peak": ALU_PEAK_TOPS, "unit": "TFLOP/s",
+                "frac": achieved / ALU_PEAK_TOPS,
+                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                "kernel": "cells_kernel (3 capacity tiers, one launch each)",
+                "kernel_ms": kms, "kernel_share_of_step": kms / ms if world == 1 else None,
+                "work_model": "W_min = 2.3e4 FP ops/cell (SURVEY.md §8(d)); peak = 148 SM x 128 lanes x 1.965 GHz "
+                              "(derived, not measured; MEASURED_PEAKS.json has no FP32 figure)"}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
+                "config": {"workload": f"{wl.name}: {wl.description}", "n": wl.n, "box": list(wl.box),
+                           "leaf_size": args.leaf or 16, "parallelism": f"seed-sharded x{world}",
+                           "l2": "flushed before every timed step (256 MiB write)", "generation_s": round(gen_s, 1)},
+                "roofline": roof,
+                "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+                "clocks": clocks, "gpu_launches": int(launches),
+                "stats": {k: stats[k] for k in ("nodes_visited", "leaves_visited", "sites_tested", "clip_tests",
+                                                 "clips", "tier_cells", "overflow_cells", "ms_bvh", "ms_cells",
+                                                 "ms_csr")},
+                "nnz": nnz_total, "empty_ratio": float(np.mean(flags_np & 1)),
+                "step_ms": [round(x, 3) for x in step_ms]}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(wl)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--n", type=int, default=None, help="override the config's size (debug only)")
+    ap.add_argument("--leaf", type=int, default=0)
+    ap.add_argument("--ref-cells", type=int, default=64, help="reference arm: cells per step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

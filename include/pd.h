@@ -58,7 +58,10 @@ enum {
     PD_STATS = 1u << 2,       /* collect traversal/clipping counters (pd_get_stats) */
     PD_ISOTROPIC = 1u << 3,   /* ablation: isotropic radius instead of the directional one */
     PD_DFS = 1u << 4,         /* ablation: depth-first LIFO traversal instead of best-first */
-    PD_AABB_SUPPORT = 1u << 6 /* tighter site test: exact AABB support max_{y in AABB} y.D (not the paper's) */
+    PD_PAPER_BOUND = 1u << 6, /* ablation: the paper's culling bounds only (no AABB-support companion) */
+    PD_COST = 1u << 7,        /* record per-cell work (pd_cell_cost): BVH nodes + leaf sites + clips */
+    PD_EXACT_NODES = 1u << 8, /* exact polytope-vs-box node test on every node the AABB tests keep */
+    PD_NO_EXACT = 1u << 9     /* never use the exact polytope-vs-box node test (pure AABB culling) */
 };
 
 /* pd_cell_flags values */
@@ -88,8 +91,10 @@ typedef struct {
     int64_t clips;             /* clips that changed the cell */
     int64_t tier_cells[3];     /* cells finished in each capacity tier */
     int64_t overflow_cells;    /* cells flagged PD_CELL_OVERFLOW */
+    int64_t queue_spills;      /* queue entries spilled to global memory */
     int64_t nnz;               /* total neighbour entries */
     double ms_bvh, ms_cells, ms_csr, ms_total; /* phase times (CUDA events) */
+    double ms_tier[3];         /* cell-kernel time per capacity tier (CUDA events) */
 } pd_stats;
 
 typedef struct pd_result pd_result;
@@ -116,6 +121,7 @@ const float* pd_face_areas(const pd_result* r);  /* nnz; aligned with pd_neighbo
 const float* pd_volumes(const pd_result* r);     /* n; 0 for EMPTY */
 const float* pd_surface(const pd_result* r);     /* n; total surface area incl. box walls */
 const uint8_t* pd_cell_flags(const pd_result* r);/* n; PD_CELL_* bits */
+const int32_t* pd_cell_cost(const pd_result* r); /* n (device); per-cell work, only with PD_COST, else NULL */
 pd_status pd_get_stats(const pd_result* r, pd_stats* s);
 void pd_free(pd_result* r);
 

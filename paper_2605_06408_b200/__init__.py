@@ -21,11 +21,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpd.so")
 
 PD_OK, PD_EINVAL, PD_EEMPTY, PD_ENONFINITE, PD_EOUTSIDE, PD_ENOMEM, PD_ECUDA, PD_ENCCL, PD_EINTERNAL = range(9)
-IN_DEVICE, OUT_HOST, STATS, ISOTROPIC, DFS, AABB_SUPPORT = 1, 2, 4, 8, 16, 64
+IN_DEVICE, OUT_HOST, STATS, ISOTROPIC, DFS, PAPER_BOUND, COST, EXACT_NODES, NO_EXACT = 1, 2, 4, 8, 16, 64, 128, 256, 512
 CELL_EMPTY, CELL_BOUNDARY, CELL_OVERFLOW, CELL_DUPLICATE, CELL_NOT_OWNED = 1, 2, 4, 8, 32
 
 EXPORTED = ["pd_build", "pd_num_cells", "pd_nnz", "pd_on_host", "pd_offsets", "pd_neighbors", "pd_face_areas",
-            "pd_volumes", "pd_surface", "pd_cell_flags", "pd_get_stats", "pd_free", "pd_slice_begin",
+            "pd_volumes", "pd_surface", "pd_cell_flags", "pd_cell_cost", "pd_get_stats", "pd_free", "pd_slice_begin",
             "pd_slice_end", "pd_morton_perm", "pd_assemble", "pd_export_slice", "pd_slice_nnz",
             "pd_strerror", "pd_error_index", "pd_last_cuda_error", "pd_abi_version", "pd_last_launch_count"]
 
@@ -49,13 +49,15 @@ class _Options(ctypes.Structure):
 class Stats(ctypes.Structure):
     _fields_ = [("cells", ctypes.c_int64), ("nodes_visited", ctypes.c_int64), ("leaves_visited", ctypes.c_int64),
                 ("sites_tested", ctypes.c_int64), ("clip_tests", ctypes.c_int64), ("clips", ctypes.c_int64),
-                ("tier_cells", ctypes.c_int64 * 3), ("overflow_cells", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("tier_cells", ctypes.c_int64 * 3), ("overflow_cells", ctypes.c_int64), ("queue_spills", ctypes.c_int64),
+                ("nnz", ctypes.c_int64),
                 ("ms_bvh", ctypes.c_double), ("ms_cells", ctypes.c_double), ("ms_csr", ctypes.c_double),
-                ("ms_total", ctypes.c_double)]
+                ("ms_total", ctypes.c_double), ("ms_tier", ctypes.c_double * 3)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
         d["tier_cells"] = list(self.tier_cells)
+        d["ms_tier"] = list(self.ms_tier)
         return d
 
 
@@ -75,7 +77,7 @@ def load_library(path: str = LIB_PATH):
     L.pd_build.argtypes = [P, P, I64, P, P, ctypes.POINTER(P)]
     for name, rt in [("pd_num_cells", I64), ("pd_nnz", I64), ("pd_on_host", ctypes.c_int),
                      ("pd_offsets", P), ("pd_neighbors", P), ("pd_face_areas", P), ("pd_volumes", P),
-                     ("pd_surface", P), ("pd_cell_flags", P), ("pd_slice_begin", I64), ("pd_slice_end", I64),
+                     ("pd_surface", P), ("pd_cell_flags", P), ("pd_cell_cost", P), ("pd_slice_begin", I64), ("pd_slice_end", I64),
                      ("pd_morton_perm", P), ("pd_slice_nnz", I64)]:
         getattr(L, name).restype = rt
         getattr(L, name).argtypes = [P]
@@ -275,6 +277,16 @@ def export_slice(d: Diagram, stream=None):
                              rn.data_ptr(), ra.data_ptr(), ctypes.byref(total), ctypes.c_void_p(stream)))
     t = int(total.value)
     return cnt, vol, surf, flg, rn[:t], ra[:t]
+
+
+def cell_cost(d: Diagram):
+    """Per-cell work counters (needs flags=COST): torch int32 CUDA tensor in original order."""
+    L = load_library()
+    ptr = L.pd_cell_cost(d.handle.ptr)
+    if not ptr:
+        raise ValueError("built without COST flag")
+    import torch
+    return torch.as_tensor(_CudaView(d.handle, ptr, (d.n,), "<i4"), device="cuda")
 
 
 def morton_perm(d: Diagram):

@@ -30,6 +30,7 @@ struct pd_result {
     int64_t slice_begin = 0, slice_end = 0, slice_nnz = 0;
     int32_t* perm = nullptr;  // device, Morton position -> original id
     int32_t* cnt = nullptr;   // device, per original id
+    int32_t* cost = nullptr;  // device, per original id (PD_COST)
     pd_stats stats;
     std::vector<void*> dev;
     std::vector<void*> host;
@@ -256,10 +257,19 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         int32_t* list_counts = A.alloc<int32_t>(4);
         int* aovf = A.alloc<int>(1);
         pd::Stats* dstats = A.alloc<pd::Stats>(1);
+        int32_t* cost = (opt.flags & PD_COST) ? A.alloc<int32_t>(n) : nullptr;
+        if (cost) ck(cudaMemsetAsync(cost, 0, sizeof(int32_t) * n, st));
         int64_t cap = std::max<int64_t>((end - begin) * 18, 1 << 16);
         int32_t* anbr = nullptr;
         float* aarea = nullptr;
         int sms = num_sms(opt.device);
+        const int spill_cap[3] = {2048, 8192, 65536};
+        size_t spill_entries = 0;
+        for (int t = 0; t < 3; ++t)
+            spill_entries = std::max(spill_entries, (size_t)pd::cells_grid_warps(t, sms) * spill_cap[t]);
+        pd::NodeChild* spill = A.alloc<pd::NodeChild>(spill_entries);
+        cudaEvent_t tev[4];
+        for (auto& e : tev) ck(cudaEventCreate(&e));
         for (int attempt = 0; attempt < 3; ++attempt) {
             anbr = A.alloc<int32_t>(cap);
             aarea = A.alloc<float>(cap);
@@ -291,7 +301,9 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.out.arena_top = counters + 4;
             P.out.arena_cap = cap;
             P.out.arena_overflow = aovf;
+            P.out.cost = cost;
             P.stats = dstats;
+            P.spill = spill;
             int64_t L = end - begin;
             for (int tier = 0; tier < 3; ++tier) {
                 P.work_counter = counters + tier;
@@ -307,8 +319,11 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
                 }
                 P.next_list = lists + (size_t)(tier & 1) * std::max<int64_t>(L, 1);
                 P.next_count = list_counts + tier;
+                P.spill_cap = spill_cap[tier];
+                ck(cudaEventRecord(tev[tier], st));
                 ck(pd::launch_cells(tier, P, st, sms, &launches));
             }
+            ck(cudaEventRecord(tev[3], st));
             unsigned long long top = 0;
             int ovf = 0;
             ck(cudaMemcpyAsync(&top, counters + 4, sizeof(top), cudaMemcpyDeviceToHost, st));
@@ -341,6 +356,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         r->flags = to_result(r, A, flags);
         r->perm = to_result(r, A, perm);
         r->cnt = to_result(r, A, cnt);
+        if (cost) r->cost = to_result(r, A, cost);
         r->slice_nnz = nnz;
         finish_outputs(r, A, opt.flags, st);
         ck(cudaEventRecord(ev[4], st));
@@ -354,6 +370,12 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         cudaEventElapsedTime(&t04, ev[0], ev[4]);
         for (auto& e : ev) cudaEventDestroy(e);
         pd_stats& s = r->stats;
+        for (int k = 0; k < 3; ++k) {
+            float tt = 0.f;
+            cudaEventElapsedTime(&tt, tev[k], tev[k + 1]);
+            s.ms_tier[k] = tt;
+        }
+        for (auto& e : tev) cudaEventDestroy(e);
         s.cells = (int64_t)hs.cells;
         s.nodes_visited = (int64_t)hs.nodes;
         s.leaves_visited = (int64_t)hs.leaves;
@@ -362,6 +384,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         s.clips = (int64_t)hs.clips;
         for (int k = 0; k < 3; ++k) s.tier_cells[k] = (int64_t)hs.tier[k];
         s.overflow_cells = (int64_t)hs.overflow;
+        s.queue_spills = (int64_t)hs.spills;
         s.nnz = nnz;
         s.ms_bvh = t01;
         s.ms_cells = t12;
@@ -400,6 +423,7 @@ const float* pd_face_areas(const pd_result* r) { return r ? r->area : nullptr; }
 const float* pd_volumes(const pd_result* r) { return r ? r->vol : nullptr; }
 const float* pd_surface(const pd_result* r) { return r ? r->surf : nullptr; }
 const uint8_t* pd_cell_flags(const pd_result* r) { return r ? r->flags : nullptr; }
+const int32_t* pd_cell_cost(const pd_result* r) { return r ? r->cost : nullptr; }
 pd_status pd_get_stats(const pd_result* r, pd_stats* s) {
     if (!r || !s) return PD_EINVAL;
     *s = r->stats;

@@ -50,10 +50,8 @@ struct __align__(16) WarpState {
     double vx[T::VMAX], vy[T::VMAX], vz[T::VMAX];
     uint32_t vt[T::VMAX];         // triplet a | b << 10 | c << 20, CCW seen from outside
     int32_t pid[T::PMAX];         // >= 0 Morton index of the neighbour site; -1-k box wall k
-    int32_t qlink[T::QMAX];
-    float qd[T::QMAX];
-    float qdw[T::QMAX];
-    uint8_t qallow[T::QMAX];
+    float4 qlo[T::QMAX];          // priority queue: the pushed child records (lo, maxw), (hi, link)
+    float4 qhi[T::QMAX];
     uint16_t rem[T::VMAX];        // removed-vertex slots of the current clip
     uint32_t omask[T::VC];        // outside-vertex ballots of the current clip
     uint32_t qmask[T::QC];        // alive-entry ballots of the current pop
@@ -87,6 +85,17 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 }
 
 __device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(FULL, v, src); }
+__device__ __forceinline__ float4 shfl_f4(float4 v, int src) {
+    return make_float4(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src), __shfl_sync(FULL, v.z, src),
+                       __shfl_sync(FULL, v.w, src));
+}
+// Exact node tests switch on once a cell has visited this many nodes (heavy cells), or always with
+// PD_EXACT_NODES; PD_NO_EXACT disables them.
+constexpr unsigned long long kExactAfterNodes = 64;
+__device__ __forceinline__ bool exact_on(unsigned flags, unsigned long long visited) {
+    if (flags & PD_NO_EXACT) return false;
+    return (flags & PD_EXACT_NODES) || visited > kExactAfterNodes;
+}
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
@@ -98,7 +107,7 @@ enum { ST_OK = 0, ST_EMPTY = 1, ST_OVERFLOW = 2, ST_DUP = 3 };
 enum { CLIP_NONE = 0, CLIP_DONE = 1, CLIP_EMPTY = 2, CLIP_OVF = 3 };
 
 struct Counters {
-    unsigned long long nodes, leaves, sites, tests, clips;
+    unsigned long long nodes, leaves, sites, tests, clips, spills;
 };
 
 // Per-warp register state (identical in all lanes).
@@ -126,38 +135,42 @@ __device__ __forceinline__ float dir_r2(const Cell& c, unsigned allow, bool iso)
     return r2;
 }
 
-// Node test: lower bound on d_ij over B is d/2 + min(0, w_i - w_max)/(2d);
-// cull iff it exceeds r, i.e. q - 2 r d > 0 with q = d^2 + min(0, w_i - w_max).  FP32 with a 1e-5
-// relative margin so that rounding can only keep a node, never cull a needed one.
-__device__ __forceinline__ float node_key(const Cell& c, float4 lo_w, float4 hi_l, bool iso, float& d_out,
-                                          float& dw_out, unsigned& allow_out, bool& culled) {
-    float gx = fmaxf(fmaxf(lo_w.x - c.fpx, c.fpx - hi_l.x), 0.f);
-    float gy = fmaxf(fmaxf(lo_w.y - c.fpy, c.fpy - hi_l.y), 0.f);
-    float gz = fmaxf(fmaxf(lo_w.z - c.fpz, c.fpz - hi_l.z), 0.f);
-    float d2 = gx * gx + gy * gy + gz * gz;
-    unsigned allow = (hi_l.x >= c.fpx ? 1u : 0u) | (lo_w.x <= c.fpx ? 2u : 0u) | (hi_l.y >= c.fpy ? 4u : 0u) |
-                     (lo_w.y <= c.fpy ? 8u : 0u) | (hi_l.z >= c.fpz ? 16u : 0u) | (lo_w.z <= c.fpz ? 32u : 0u);
-    float d = sqrtf(d2);
-    float dw = fminf(0.f, c.fpw - lo_w.w);
+// Node test.  Two sound culls, a node is discarded if EITHER holds (FP32, 1e-5 relative margins so
+// rounding can only keep a node):
+//  (1) the paper's: the lower bound d/2 + min(0, w_i - w_max)/(2d) on d_ij over
+//      the box exceeds the directional radius r of the octants the box occupies, i.e.
+//      d^2 + min(0, w_i - w_max) - 2 r d > 0;
+//  (2) a companion bound from the same cell AABB: for p_j in B and y in the cell,
+//      y.D <= H = sum_k max(lo_k a_k, lo_k b_k, hi_k a_k, hi_k b_k) with D_k in [a_k, b_k] (the box
+//      minus p_i), while the plane offset is (|D|^2 + w_i - w_j)/2 >= (d^2 + w_i - w_max)/2;
+//      so no plane of B cuts the cell if d^2 + w_i - w_max > 2H.  (2) is never looser than (1) for
+//      small far boxes (Cauchy-Schwarz) and is disabled by PD_PAPER_BOUND / PD_ISOTROPIC.
+// Returns the Alg. 1 priority delta = NodeSqrDist - r^2 (+ the weight term): order only.
+__device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi_l, unsigned flags, bool& culled) {
+    const bool iso = (flags & PD_ISOTROPIC) != 0;
+    const bool paper = (flags & (PD_PAPER_BOUND | PD_ISOTROPIC)) != 0;
+    float a0 = lo_w.x - c.fpx, a1 = lo_w.y - c.fpy, a2 = lo_w.z - c.fpz;
+    float b0 = hi_l.x - c.fpx, b1 = hi_l.y - c.fpy, b2 = hi_l.z - c.fpz;
+    float g0 = fmaxf(fmaxf(a0, -b0), 0.f), g1 = fmaxf(fmaxf(a1, -b1), 0.f), g2 = fmaxf(fmaxf(a2, -b2), 0.f);
+    float d2 = g0 * g0 + g1 * g1 + g2 * g2;
+    unsigned allow = (b0 >= 0.f ? 1u : 0u) | (a0 <= 0.f ? 2u : 0u) | (b1 >= 0.f ? 4u : 0u) | (a1 <= 0.f ? 8u : 0u) |
+                     (b2 >= 0.f ? 16u : 0u) | (a2 <= 0.f ? 32u : 0u);
+    float dw = c.fpw - lo_w.w;
+    float dwn = fminf(0.f, dw);
     float r2 = dir_r2(c, allow, iso);
-    float r = sqrtf(r2);
-    float lin = d2 + dw - 2.f * r * d;
-    culled = lin > 1e-5f * (d2 - dw + 2.f * r * d);
-    float key = d2 + dw - r2;  // Alg. 1 priority delta = NodeSqrDist - r^2 (+ weight term)
-    d_out = d;
-    dw_out = dw;
-    allow_out = allow;
-    return key;
-}
-
-__device__ __forceinline__ float node_key_stored(const Cell& c, float d, float dw, unsigned allow, bool iso,
-                                                 bool& culled) {
-    float r2 = dir_r2(c, allow, iso);
-    float r = sqrtf(r2);
-    float d2 = d * d;
-    float lin = d2 + dw - 2.f * r * d;
-    culled = lin > 1e-5f * (d2 - dw + 2.f * r * d);
-    return d2 + dw - r2;
+    float rd = sqrtf(r2 * d2);
+    culled = d2 + dwn - 2.f * rd > 1e-5f * (d2 - dwn + 2.f * rd);
+    if (!paper) {
+        float h0 = fmaxf(fmaxf(c.flo[0] * a0, c.flo[0] * b0), fmaxf(c.fhi[0] * a0, c.fhi[0] * b0));
+        float h1 = fmaxf(fmaxf(c.flo[1] * a1, c.flo[1] * b1), fmaxf(c.fhi[1] * a1, c.fhi[1] * b1));
+        float h2 = fmaxf(fmaxf(c.flo[2] * a2, c.flo[2] * b2), fmaxf(c.fhi[2] * a2, c.fhi[2] * b2));
+        float H = h0 + h1 + h2;
+        float mag = fmaxf(fabsf(c.flo[0]), c.fhi[0]) * fmaxf(fabsf(a0), fabsf(b0)) +
+                    fmaxf(fabsf(c.flo[1]), c.fhi[1]) * fmaxf(fabsf(a1), fabsf(b1)) +
+                    fmaxf(fabsf(c.flo[2]), c.fhi[2]) * fmaxf(fabsf(a2), fabsf(b2));
+        culled |= d2 + dw - 2.f * H > 1e-5f * (d2 + fabsf(dw) + 2.f * mag);
+    }
+    return d2 + dwn - r2;
 }
 
 template <class T>
@@ -328,12 +341,13 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double nx, 
     return CLIP_DONE;
 }
 
-// Site test in FP64: cull iff d_ij > r, i.e. q > 0 and q^2 > 4 r^2 |D|^2,
-// q = |D|^2 + w_i - w_j.  With PD_AABB_SUPPORT the (tighter) exact support of the cell AABB in
-// direction D replaces r |D|.
+// Site test in FP64: cull iff the plane y.D <= q/2 (q = |D|^2 + w_i - w_j)
+// cannot cut the cell.  Paper: d_ij = q/(2|D|) > r with r the directional radius of p_j's octant,
+// i.e. q > 0 and q^2 > 4 r^2 |D|^2.  Default: the exact support of the cell AABB in direction D,
+// h = sum_k max(lo_k D_k, hi_k D_k) <= r |D| (Cauchy-Schwarz), cull iff q/2 > h: never looser.
 __device__ __forceinline__ bool site_culled(const Cell& c, double Dx, double Dy, double Dz, double q, double D2,
                                             unsigned flags) {
-    if (flags & PD_AABB_SUPPORT) {
+    if (!(flags & (PD_PAPER_BOUND | PD_ISOTROPIC))) {
         double h = Dx * (Dx >= 0 ? (double)c.fhi[0] : (double)c.flo[0]) + Dy * (Dy >= 0 ? (double)c.fhi[1] : (double)c.flo[1]) +
                    Dz * (Dz >= 0 ? (double)c.fhi[2] : (double)c.flo[2]);
         return 0.5 * q > h + 1e-9 * (fabs(h) + D2);
@@ -348,6 +362,33 @@ __device__ __forceinline__ bool site_culled(const Cell& c, double Dx, double Dy,
         r2 = hx * hx + hy * hy + hz * hz;
     }
     return q > 0 && q * q > 4.0 * r2 * D2 * (1.0 + 1e-9);
+}
+
+// Exact polytope-vs-box node test (not in the paper; strictly tighter than any AABB bound).  The
+// plane of p_j (D = p_j - p_i) cuts the cell iff some vertex v has v.D - |D|^2/2 > (w_i - w_j)/2.
+// Over all p_j in the box, D_k in [a_k, b_k] and w_j <= w_max, and
+//   max_{D in box} (v.D - |D|^2/2) = sum_k (v_k c_k - c_k^2/2),  c_k = clamp(v_k, a_k, b_k),
+// (a separable concave maximisation), so the node is culled iff for every vertex that sum is
+// <= (w_i - w_max)/2.  Lanes = vertices, FP64, relative margin so rounding only keeps nodes.
+template <class T>
+__device__ __noinline__ bool node_exact_culled(const WarpState<T>& S, const Cell& c, int lane, float4 lo_w, float4 hi_l) {
+    const double a0 = (double)lo_w.x - c.px, a1 = (double)lo_w.y - c.py, a2 = (double)lo_w.z - c.pz;
+    const double b0 = (double)hi_l.x - c.px, b1 = (double)hi_l.y - c.py, b2 = (double)hi_l.z - c.pz;
+    const double rhs = 0.5 * (c.pw - (double)lo_w.w);
+    double best = -1e300, mag = 0.0;
+    for (int s = lane; s < c.nv; s += 32) {
+        double vx = S.vx[s], vy = S.vy[s], vz = S.vz[s];
+        double cx = fmin(fmax(vx, a0), b0), cy = fmin(fmax(vy, a1), b1), cz = fmin(fmax(vz, a2), b2);
+        double f = cx * (vx - 0.5 * cx) + cy * (vy - 0.5 * cy) + cz * (vz - 0.5 * cz);
+        best = fmax(best, f);
+        mag = fmax(mag, fabs(cx * vx) + fabs(cy * vy) + fabs(cz * vz));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        best = fmax(best, __shfl_xor_sync(FULL, best, o));
+        mag = fmax(mag, __shfl_xor_sync(FULL, mag, o));
+    }
+    return best < rhs - 1e-12 * (mag + fabs(rhs));
 }
 
 template <class T>
@@ -413,41 +454,55 @@ __device__ __noinline__ int process_leaf(WarpState<T>& S, Cell& c, int lane, int
     return ST_OK;
 }
 
-// Best-first traversal (Alg. 1).
+// Best-first traversal (Alg. 1).  Queue entries are the pushed child records;
+// when the on-chip queue is full, entries spill to a per-warp stack in global memory (order is
+// relaxed, correctness is not affected) and are refilled when the on-chip queue drains.
 template <class T>
-__device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P, Counters& cnt) {
-    const bool iso = (P.flags & PD_ISOTROPIC) != 0;
+__device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P, Counters& cnt, NodeChild* spill,
+                        int spill_cap) {
     const bool dfs = (P.flags & PD_DFS) != 0;
     int node = __float_as_int(__ldg(&P.root->hi_l.w));
     bool have = true;
+    int ns = 0;  // spilled entries
+    const unsigned long long nodes0 = cnt.nodes;
     c.nq = 0;
     for (;;) {
         if (have) {
             while (node >= 0) {  // descend (Alg. 1 lines 4-18)
                 cnt.nodes++;
-                float key = INFINITY, d = 0.f, dw = 0.f;
-                unsigned allow = 0;
+                float key = INFINITY;
                 bool culled = true;
-                int link = 0;
+                float4 lo_w = make_float4(0, 0, 0, 0), hi_l = make_float4(0, 0, 0, 0);
                 if (lane < 2) {
                     const NodeChild* ch = &P.nodes[node].c[lane];
-                    float4 lo_w = __ldg(&ch->lo_w), hi_l = __ldg(&ch->hi_l);
-                    link = __float_as_int(hi_l.w);
-                    key = node_key(c, lo_w, hi_l, iso, d, dw, allow, culled);
+                    lo_w = __ldg(&ch->lo_w);
+                    hi_l = __ldg(&ch->hi_l);
+                    key = node_test(c, lo_w, hi_l, P.flags, culled);
                 }
                 bool c0 = __shfl_sync(FULL, culled, 0), c1 = __shfl_sync(FULL, culled, 1);
+                if (exact_on(P.flags, cnt.nodes - nodes0)) {
+                    float4 l0 = shfl_f4(lo_w, 0), h0 = shfl_f4(hi_l, 0), l1 = shfl_f4(lo_w, 1), h1 = shfl_f4(hi_l, 1);
+                    if (!c0) c0 = node_exact_culled(S, c, lane, l0, h0);
+                    if (!c1) c1 = node_exact_culled(S, c, lane, l1, h1);
+                    if (lane == 0) culled = c0;
+                    if (lane == 1) culled = c1;
+                }
                 if (c0 && c1) { have = false; break; }
                 float k0 = __shfl_sync(FULL, key, 0), k1 = __shfl_sync(FULL, key, 1);
                 int near = (!c0 && (c1 || k0 <= k1)) ? 0 : 1;
                 int far = 1 - near;
                 bool cfar = far ? c1 : c0;
-                int lnear = __shfl_sync(FULL, link, near);
+                int lnear = __shfl_sync(FULL, __float_as_int(hi_l.w), near);
                 if (!cfar) {
-                    if (c.nq >= T::QMAX) return ST_OVERFLOW;
-                    if (lane == far) {
-                        S.qlink[c.nq] = link; S.qd[c.nq] = d; S.qdw[c.nq] = dw; S.qallow[c.nq] = (uint8_t)allow;
+                    if (c.nq < T::QMAX) {
+                        if (lane == far) { S.qlo[c.nq] = lo_w; S.qhi[c.nq] = hi_l; }
+                        c.nq++;
+                    } else {
+                        if (ns >= spill_cap) return ST_OVERFLOW;
+                        if (lane == far) { spill[ns].lo_w = lo_w; spill[ns].hi_l = hi_l; }
+                        ns++;
+                        cnt.spills++;
                     }
-                    c.nq++;
                 }
                 node = lnear;
             }
@@ -460,19 +515,34 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         }
         // pop (Alg. 1 lines 21-31): re-validate every queued entry against the shrunk cell
         __syncwarp();
+        if (c.nq == 0 && ns > 0) {  // refill from the spill stack
+            __threadfence_block();
+            int m = min(ns, T::QMAX);
+            for (int t = lane; t < m; t += 32) {
+                NodeChild e = spill[ns - m + t];
+                S.qlo[t] = e.lo_w;
+                S.qhi[t] = e.hi_l;
+            }
+            ns -= m;
+            c.nq = m;
+            __syncwarp();
+        }
         if (c.nq == 0) return ST_OK;
         if (dfs) {
             bool ok = false;
             while (c.nq > 0 && !ok) {
                 int t = c.nq - 1;
                 bool culled;
-                node_key_stored(c, S.qd[t], S.qdw[t], S.qallow[t], iso, culled);
-                node = S.qlink[t];
+                node_test(c, S.qlo[t], S.qhi[t], P.flags, culled);
+                node = __float_as_int(S.qhi[t].w);
                 c.nq--;
                 ok = !culled;
             }
             __syncwarp();
-            if (!ok) return ST_OK;
+            if (!ok) {
+                if (ns > 0) continue;
+                return ST_OK;
+            }
             have = true;
             continue;
         }
@@ -483,7 +553,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             bool al = false;
             if (s < c.nq) {
                 bool culled;
-                float k = node_key_stored(c, S.qd[s], S.qdw[s], S.qallow[s], iso, culled);
+                float k = node_test(c, S.qlo[s], S.qhi[s], P.flags, culled);
                 al = !culled;
                 if (al && ford(k) < bestk) { bestk = ford(k); bests = s; }
             }
@@ -492,30 +562,35 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         }
         __syncwarp();
         int gk = __reduce_min_sync(FULL, bestk);
-        if (gk == 0x7fffffff) { c.nq = 0; return ST_OK; }
+        if (gk == 0x7fffffff) {
+            c.nq = 0;
+            have = false;
+            if (ns > 0) continue;
+            return ST_OK;
+        }
         unsigned lead = __ballot_sync(FULL, bestk == gk);
         int bslot = __shfl_sync(FULL, bests, __ffs(lead) - 1);
-        node = S.qlink[bslot];
+        node = __float_as_int(S.qhi[bslot].w);
+        bool popped_dead = exact_on(P.flags, cnt.nodes - nodes0) && node_exact_culled(S, c, lane, S.qlo[bslot], S.qhi[bslot]);
         // compact: keep alive entries except the popped one
         int base = 0;
         for (int ch = 0; ch < qch; ++ch) {
-            {
-                int s = ch * 32 + lane;
-                bool keep = ((S.qmask[ch] >> lane) & 1u) && s != bslot;
-                unsigned km = __ballot_sync(FULL, keep);
-                int l = 0; float dd = 0.f, ww = 0.f; uint8_t aa = 0;
-                if (keep) { l = S.qlink[s]; dd = S.qd[s]; ww = S.qdw[s]; aa = S.qallow[s]; }
-                __syncwarp();
-                if (keep) {
-                    int dst = base + __popc(km & lanemask_lt());
-                    S.qlink[dst] = l; S.qd[dst] = dd; S.qdw[dst] = ww; S.qallow[dst] = aa;
-                }
-                __syncwarp();
-                base += __popc(km);
+            int s = ch * 32 + lane;
+            bool keep = ((S.qmask[ch] >> lane) & 1u) && s != bslot;
+            unsigned km = __ballot_sync(FULL, keep);
+            float4 lo = make_float4(0, 0, 0, 0), hi = make_float4(0, 0, 0, 0);
+            if (keep) { lo = S.qlo[s]; hi = S.qhi[s]; }
+            __syncwarp();
+            if (keep) {
+                int dst = base + __popc(km & lanemask_lt());
+                S.qlo[dst] = lo;
+                S.qhi[dst] = hi;
             }
+            __syncwarp();
+            base += __popc(km);
         }
         c.nq = base;
-        have = true;
+        have = !popped_dead;
     }
 }
 
@@ -662,7 +737,9 @@ __global__ void __launch_bounds__(T::WARPS * 32) cells_kernel(CellParams P, int 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpState<T>& S = reinterpret_cast<WarpState<T>*>(smem_raw)[wid];
     const int64_t total = P.list ? (int64_t)(*P.list_count) : P.count;
-    Counters cnt = {0, 0, 0, 0, 0};
+    Counters cnt = {0, 0, 0, 0, 0, 0};
+    const int gw = blockIdx.x * T::WARPS + wid;
+    NodeChild* spill = P.spill + (size_t)gw * P.spill_cap;
     unsigned long long ncells = 0, novf = 0;
     constexpr int BATCH = 4;
     for (;;) {
@@ -674,13 +751,14 @@ __global__ void __launch_bounds__(T::WARPS * 32) cells_kernel(CellParams P, int 
             int64_t idx = b0 + b;
             int s = P.list ? P.list[idx] : (int)(P.begin + idx);
             Cell c;
+            const Counters before = cnt;
             float4 site = __ldg(&P.sites[s]);
             c.fpx = site.x; c.fpy = site.y; c.fpz = site.z; c.fpw = site.w;
             c.px = site.x; c.py = site.y; c.pz = site.z; c.pw = site.w;
             c.self = s;
             c.self_orig = __ldg(&P.perm[s]);
             init_cell(S, c, lane, P);
-            int st = traverse(S, c, lane, P, cnt);
+            int st = traverse(S, c, lane, P, cnt, spill, P.spill_cap);
             __syncwarp();
             if (st == ST_OVERFLOW && !P.last_tier) {
                 if (lane == 0) {
@@ -692,6 +770,10 @@ __global__ void __launch_bounds__(T::WARPS * 32) cells_kernel(CellParams P, int 
             if (st == ST_OVERFLOW) novf++;
             finalize(S, c, lane, P, st);
             ncells++;
+            if ((P.flags & PD_COST) && lane == 0) {
+                unsigned long long w = (cnt.nodes - before.nodes) + (cnt.sites - before.sites) + 8 * (cnt.clips - before.clips);
+                P.out.cost[c.self_orig] = (int32_t)min(w, 0x7fffffffull);
+            }
             __syncwarp();
         }
     }
@@ -704,19 +786,24 @@ __global__ void __launch_bounds__(T::WARPS * 32) cells_kernel(CellParams P, int 
         atomicAdd(&P.stats->cells, ncells);
         atomicAdd(&P.stats->tier[tier], ncells);
         atomicAdd(&P.stats->overflow, novf);
+        atomicAdd(&P.stats->spills, cnt.spills);
     }
+}
+
+template <class T>
+int tier_grid(int num_sms) {
+    size_t smem = sizeof(WarpState<T>) * T::WARPS;
+    cudaFuncSetAttribute(cells_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cells_kernel<T>, T::WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    return num_sms * per_sm;
 }
 
 template <class T>
 cudaError_t launch_tier(const CellParams& p, int tier, cudaStream_t st, int num_sms) {
     size_t smem = sizeof(WarpState<T>) * T::WARPS;
-    cudaError_t e = cudaFuncSetAttribute(cells_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cells_kernel<T>, T::WARPS * 32, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-    int grid = num_sms * per_sm;
+    int grid = tier_grid<T>(num_sms);
     cells_kernel<T><<<grid, T::WARPS * 32, smem, st>>>(p, tier);
     return cudaGetLastError();
 }
@@ -730,10 +817,10 @@ cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num
     return launch_tier<Tier3>(p, 2, st, num_sms);
 }
 
-size_t cells_smem_per_warp(int tier) {
-    if (tier == 0) return sizeof(WarpState<Tier1>);
-    if (tier == 1) return sizeof(WarpState<Tier2>);
-    return sizeof(WarpState<Tier3>);
+int cells_grid_warps(int tier, int num_sms) {
+    if (tier == 0) return tier_grid<Tier1>(num_sms) * Tier1::WARPS;
+    if (tier == 1) return tier_grid<Tier2>(num_sms) * Tier2::WARPS;
+    return tier_grid<Tier3>(num_sms) * Tier3::WARPS;
 }
 
 }  // namespace pd

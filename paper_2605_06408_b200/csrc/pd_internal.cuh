@@ -41,10 +41,11 @@ struct CellOut {
     unsigned long long* arena_top;  // atomic bump pointer (entries)
     int64_t arena_cap;
     int* arena_overflow;            // set to 1 when a row did not fit
+    int32_t* cost;                  // optional per-cell work (PD_COST)
 };
 
 struct Stats {  // device counters (PD_STATS)
-    unsigned long long nodes, leaves, sites, clip_tests, clips, cells, tier[3], overflow;
+    unsigned long long nodes, leaves, sites, clip_tests, clips, cells, tier[3], overflow, spills;
 };
 
 struct CellParams {
@@ -66,8 +67,11 @@ struct CellParams {
     int last_tier;
     CellOut out;
     Stats* stats;
+    NodeChild* spill;   // per-warp queue spill stacks (global memory)
+    int spill_cap;      // entries per warp
 };
 
 cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches);
+int cells_grid_warps(int tier, int num_sms);
 
 }  // namespace pd

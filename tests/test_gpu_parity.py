@@ -65,7 +65,7 @@ def test_leaf_sizes_identical(leaf):
     assert np.allclose(ref.volumes, g.volumes, rtol=1e-6, atol=0)
 
 
-@pytest.mark.parametrize("flag", [pd.ISOTROPIC, pd.DFS, pd.AABB_SUPPORT])
+@pytest.mark.parametrize("flag", [pd.ISOTROPIC, pd.DFS, pd.PAPER_BOUND])
 def test_ablations_neutral(flag):
     """Culling / traversal variants change the work, not the diagram."""
     wl = pdgen.make("C3", n=8009)
