@@ -76,7 +76,7 @@ enum {
 typedef struct {
     int device;        /* CUDA device ordinal */
     void* stream;      /* cudaStream_t (NULL = default stream) */
-    int leaf_size;     /* BVH leaf size l, 1..32 (0 = default 16); PAPER.md:527 uses 17 / 10 */
+    int leaf_size;     /* BVH leaf size l, 1..32 (0 = default 32); PAPER.md:527 uses 17 / 10 */
     unsigned flags;    /* PD_* flags above */
     int shard_rank;    /* sharded build: this rank's slice of the Morton order (0 when world=1) */
     int shard_world;   /* number of slices (0 or 1 = whole diagram) */

@@ -64,11 +64,12 @@ class Stats(ctypes.Structure):
 _lib = None
 
 
-def load_library(path: str = LIB_PATH):
-    """Load libpd.so; raises (never falls back) if it is missing."""
+def load_library(path: str | None = None):
+    """Load libpd.so (or $PD_LIB, an alternative in-tree build); raises (never falls back) if missing."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("PD_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise RuntimeError(f"{path} not built: run `python -m paper_2605_06408_b200.build` (no CPU fallback)")
     L = ctypes.CDLL(path)

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpd.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-Wno-deprecated-declarations", "--expt-relaxed-constexpr",
          "-Xcudafe", "--diag_suppress=177"]
 
 
@@ -33,25 +33,27 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every csrc/*.cu for sm_100a and link libpd.so (or `out`, with extra -D defines)."""
+    LIB_OUT = out or LIB
+    if not force and os.path.exists(LIB_OUT):
+        t = os.path.getmtime(LIB_OUT)
         if all(os.path.getmtime(d) <= t for d in deps()):
-            return LIB
-    objdir = os.path.join(HERE, "build")
+            return LIB_OUT
+    objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [nvcc()] + ARCH + FLAGS + ["-c", src, "-o", obj]
+        cmd = [nvcc()] + ARCH + FLAGS + ["-D" + d for d in defines] + ["-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)
         objs.append(obj)
-    cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs + ["-lcudart"]
+    cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB_OUT + ".tmp"] + objs + ["-lcudart"]
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(LIB_OUT + ".tmp", LIB_OUT)
+    return LIB_OUT
 
 
 if __name__ == "__main__":

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -147,7 +148,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
     if (box)
         for (int k = 0; k < 3; ++k)
             if (!(box->lo[k] < box->hi[k]) || !std::isfinite(box->lo[k]) || !std::isfinite(box->hi[k])) return PD_EINVAL;
-    int leaf = opt.leaf_size > 0 ? opt.leaf_size : 16;
+    int leaf = opt.leaf_size > 0 ? opt.leaf_size : 32;
     if (leaf > 32) return PD_EINVAL;
     int world = opt.shard_world > 1 ? opt.shard_world : 1;
     int rank = world > 1 ? opt.shard_rank : 0;
@@ -238,9 +239,12 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         sc.blo = A.alloc<float4>(ni);
         sc.bhi = A.alloc<float4>(ni);
         pd::Bvh bvh;
-        bvh.nodes = A.alloc<pd::NodeRec>(ni);
+        sc.max_wide = (int)std::min<int64_t>(2 * n / leaf + 2, ni + 1);
+        bvh.nodes = A.alloc<pd::WideNode>(sc.max_wide);
+        sc.tasks[0] = A.alloc<int2>(sc.max_wide);
+        sc.tasks[1] = A.alloc<int2>(sc.max_wide);
+        sc.counters = A.alloc<int>(4);
         bvh.root = A.alloc<pd::NodeChild>(1);
-        bvh.n_internal = (int)(n - 1);
         ck(pd::bvh_topology(keys_s, sorted, (int)n, leaf, sc, bvh, st, &launches));
         ck(cudaEventRecord(ev[1], st));
         // ---- cells
@@ -304,6 +308,10 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.out.cost = cost;
             P.stats = dstats;
             P.spill = spill;
+            {
+                const char* ev = getenv("PD_EXACT_AFTER");  // tuning knob (default 200)
+                P.exact_after = ev ? atoi(ev) : 200;
+            }
             int64_t L = end - begin;
             for (int tier = 0; tier < 3; ++tier) {
                 P.work_counter = counters + tier;

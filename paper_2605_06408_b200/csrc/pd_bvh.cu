@@ -158,46 +158,85 @@ __global__ void k_refit(const float4* __restrict__ s, int n, const int2* __restr
     }
 }
 
-// Pack the child records each internal node stores for its two children; children with <= l
-// sites become leaf-range links (the collapse of PAPER.md:527's leaf size l).
-__global__ void k_records(const float4* __restrict__ s, int n, int leaf, const int2* __restrict__ child,
-                          const int2* __restrict__ range, const float4* __restrict__ blo, const float4* __restrict__ bhi,
-                          NodeRec* __restrict__ rec, NodeChild* __restrict__ root) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n - 1) return;
-    int2 c = child[i];
-    int2 r = range[i];
-    int gamma = c.x < 0 ? ~c.x : range[c.x].y;  // left child covers [r.x, gamma]
-    NodeRec out;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        int ch = q ? c.y : c.x;
-        int first = q ? gamma + 1 : r.x;
-        int last = q ? r.y : gamma;
-        int cnt = last - first + 1;
+__device__ __forceinline__ float box_area(float4 lo, float4 hi) {
+    float dx = hi.x - lo.x, dy = hi.y - lo.y, dz = hi.z - lo.z;
+    return dx * dy + dy * dz + dz * dx;
+}
+
+// Collapse the binary LBVH into 8-wide nodes, one level of wide nodes per launch.  Task (b, w):
+// wide node w covers binary subtree b.  Its children start as b's two children; the internal child
+// (more than l sites) with the largest surface area is replaced by its two children until there
+// are 8.  Children with <= l sites become leaf-range links (the collapse of PAPER.md:527's leaf
+// size l); larger ones become new wide nodes (next level's tasks).
+__global__ void k_collapse(const int2* __restrict__ tasks, int ntask, const int2* __restrict__ child,
+                           const int2* __restrict__ range, const float4* __restrict__ blo, const float4* __restrict__ bhi,
+                           const float4* __restrict__ s, int leaf, WideNode* __restrict__ wide, int* counters,
+                           int2* __restrict__ tasks_out) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntask) return;
+    int2 task = tasks[t];
+    int ref[WIDE];
+    int2 c0 = child[task.x];
+    ref[0] = c0.x;
+    ref[1] = c0.y;
+    int m = 2;
+    while (m < WIDE) {
+        int best = -1;
+        float bestA = -1.f;
+        for (int k = 0; k < m; ++k) {
+            int r = ref[k];
+            if (r < 0) continue;
+            int2 rg = range[r];
+            if (rg.y - rg.x + 1 <= leaf) continue;
+            float A = box_area(blo[r], bhi[r]);
+            if (A > bestA) { bestA = A; best = k; }
+        }
+        if (best < 0) break;
+        int2 cc = child[ref[best]];
+        ref[best] = cc.x;
+        ref[m++] = cc.y;
+    }
+    WideNode out;
+    for (int k = 0; k < WIDE; ++k) {
         float4 a, b;
         int link;
-        if (ch < 0) {
-            a = s[~ch];
+        if (k >= m) {
+            a = make_float4(INFINITY, INFINITY, INFINITY, -INFINITY);
+            b = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+            link = EMPTY_LINK;
+        } else if (ref[k] < 0) {
+            a = s[~ref[k]];
             b = a;
-            link = leaf_link(~ch, 1);
+            link = leaf_link(~ref[k], 1);
         } else {
-            a = blo[ch];
-            b = bhi[ch];
-            link = cnt <= leaf ? leaf_link(first, cnt) : ch;
+            int r = ref[k];
+            int2 rg = range[r];
+            int cnt = rg.y - rg.x + 1;
+            a = blo[r];
+            b = bhi[r];
+            if (cnt <= leaf) {
+                link = leaf_link(rg.x, cnt);
+            } else {
+                link = atomicAdd(&counters[0], 1);
+                int q = atomicAdd(&counters[1], 1);
+                tasks_out[q] = make_int2(r, link);
+            }
         }
-        out.c[q].lo_w = a;
-        out.c[q].hi_l = make_float4(b.x, b.y, b.z, __int_as_float(link));
+        out.c[k].lo_w = a;
+        out.c[k].hi_l = make_float4(b.x, b.y, b.z, __int_as_float(link));
     }
-    rec[i] = out;
-    if (i == 0) {
-        float4 lo = make_float4(fminf(out.c[0].lo_w.x, out.c[1].lo_w.x), fminf(out.c[0].lo_w.y, out.c[1].lo_w.y),
-                                fminf(out.c[0].lo_w.z, out.c[1].lo_w.z), fmaxf(out.c[0].lo_w.w, out.c[1].lo_w.w));
-        int rl = n <= leaf ? leaf_link(0, n) : 0;
-        root->lo_w = lo;
-        root->hi_l = make_float4(fmaxf(out.c[0].hi_l.x, out.c[1].hi_l.x), fmaxf(out.c[0].hi_l.y, out.c[1].hi_l.y),
-                                 fmaxf(out.c[0].hi_l.z, out.c[1].hi_l.z), __int_as_float(rl));
-    }
+    wide[task.y] = out;
+}
+
+__global__ void k_root(const float4* __restrict__ blo, const float4* __restrict__ bhi, int n, int leaf,
+                       NodeChild* root, int2* tasks, int* counters) {
+    float4 lo = blo[0], hi = bhi[0];
+    int link = n <= leaf ? leaf_link(0, n) : 0;
+    root->lo_w = lo;
+    root->hi_l = make_float4(hi.x, hi.y, hi.z, __int_as_float(link));
+    tasks[0] = make_int2(0, 0);
+    counters[0] = 1;  // wide node 0 = the root's node
+    counters[1] = 0;
 }
 
 __global__ void k_root_single(NodeChild* root) {
@@ -252,8 +291,28 @@ cudaError_t bvh_topology(const uint64_t* keys_sorted, const float4* sorted, int 
     k_karras<<<blocks(n - 1, 256), 256, 0, st>>>(keys_sorted, n, sc.child, sc.range, sc.parent_int, sc.parent_leaf);
     cudaMemsetAsync(sc.visit, 0, sizeof(int) * (size_t)(n - 1), st);
     k_refit<<<blocks(n, 256), 256, 0, st>>>(sorted, n, sc.child, sc.parent_int, sc.parent_leaf, sc.visit, sc.blo, sc.bhi);
-    k_records<<<blocks(n - 1, 256), 256, 0, st>>>(sorted, n, leaf, sc.child, sc.range, sc.blo, sc.bhi, out.nodes, out.root);
+    k_root<<<1, 1, 0, st>>>(sc.blo, sc.bhi, n, leaf, out.root, sc.tasks[0], sc.counters);
     *launches += 3;
+    out.n_wide = 0;
+    out.levels = 0;
+    if (n <= leaf) return cudaGetLastError();
+    // level-synchronous collapse: the host reads each level's task count (one small sync per level)
+    int ntask = 1, cur = 0;
+    while (ntask > 0) {
+        k_collapse<<<blocks(ntask, 128), 128, 0, st>>>(sc.tasks[cur], ntask, sc.child, sc.range, sc.blo, sc.bhi, sorted,
+                                                        leaf, out.nodes, sc.counters, sc.tasks[cur ^ 1]);
+        ++*launches;
+        ++out.levels;
+        int h[2];
+        cudaMemcpyAsync(h, sc.counters, sizeof(h), cudaMemcpyDeviceToHost, st);
+        cudaMemsetAsync(sc.counters + 1, 0, sizeof(int), st);
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return e;
+        out.n_wide = h[0];
+        if (h[0] > sc.max_wide) return cudaErrorInvalidValue;
+        ntask = h[1];
+        cur ^= 1;
+    }
     return cudaGetLastError();
 }
 

@@ -15,6 +15,9 @@ struct BvhScratch {
     int* visit = nullptr;       // n-1
     float4* blo = nullptr;      // n-1
     float4* bhi = nullptr;      // n-1
+    int2* tasks[2] = {nullptr, nullptr};  // collapse work lists (binary node, wide node)
+    int* counters = nullptr;    // [0] wide-node count, [1..2] task counts
+    int max_wide = 0;
 };
 
 cudaError_t bvh_pack(const float* pts, const float* w, int64_t n, const pd_box* box, float4* sites, float* box_dev,

@@ -11,13 +11,18 @@
 //     (Alg. 1); unsorted queue with min-scan pop
 //   * plane garbage collection at 85% occupancy
 // B200 design (differs from the paper's thread-per-cell, global-memory state):
-//   * a warp owns a cell; vertices (FP64 positions in site-local coordinates + plane-index triplets)
-//     and planes live in shared memory; classification is one FMA chain per lane + __ballot_sync;
+//   * a warp owns a cell; vertices (FP64 positions in site-local coordinates + plane-index triplets,
+//     plus an FP32 copy) and planes live in shared memory;
+//   * every classification runs in FP32 against a proven error margin and is certified in FP64 only
+//     when |s| is within that margin, so each decision equals the FP64 predicate's (PAPER.md:872
+//     runs FP32 only; SURVEY.md §7 "Precision");
 //   * the hole of a clip is found without the serial circular list of PAPER.md:556: a removed
 //     vertex's directed dual edge (x->y) is on the hole boundary iff no other removed vertex holds
 //     (y->x); every boundary edge independently spawns the vertex (h, x, y);
-//   * the queue is re-validated in parallel at every pop (all lanes, all entries), dropping entries
-//     the shrunk cell has made cullable;
+//   * a leaf's candidates are culled and cut-tested in parallel (lane = candidate); planes that do
+//     not cut the current cell are dropped for good (the cell only shrinks);
+//   * the queue is re-validated in parallel at every pop, and spills to global memory when full;
+//   * heavy cells switch on an exact polytope-vs-box node test;
 //   * capacity tiers: cells that outgrow the tier's on-chip arrays are handed to a larger tier.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -29,37 +34,55 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
-template <int V, int P, int Q, int W>
+#ifndef PD_EDGE_BITMAP
+#define PD_EDGE_BITMAP 0
+#endif
+
+template <int V, int P, int Q, int W, int MINB>
 struct TierCfg {
     static constexpr int VMAX = V;   // vertices
     static constexpr int PMAX = P;   // planes (<= 1024: 10-bit triplet fields)
-    static constexpr int QMAX = Q;   // priority-queue entries
+    static constexpr int QMAX = Q;   // on-chip priority-queue entries
     static constexpr int WARPS = W;  // warps per block
+    static constexpr int MIN_BLOCKS = MINB;  // __launch_bounds__ residency target (register cap)
     static constexpr int VC = V / 32;
-    static constexpr int PC = P / 32;
     static constexpr int QC = Q / 32;
+    // hole edges via an XOR bitmap over unordered plane pairs when it is small enough
+    static constexpr bool EDGE_BITMAP = PD_EDGE_BITMAP && P <= 256;
+    static constexpr int EBW = EDGE_BITMAP ? (P * P + 31) / 32 : 1;
 };
 
-using Tier1 = TierCfg<96, 64, 96, 4>;
-using Tier2 = TierCfg<384, 192, 384, 4>;
-using Tier3 = TierCfg<2048, 1024, 2048, 1>;
+#ifndef PD_T1_MINB
+#define PD_T1_MINB 5
+#endif
+using Tier1 = TierCfg<96, 64, 64, 4, PD_T1_MINB>;
+using Tier2 = TierCfg<384, 192, 256, 4, 1>;
+using Tier3 = TierCfg<2048, 1024, 1024, 1, 1>;
 
 template <class T>
 struct __align__(16) WarpState {
-    double4 pl[T::PMAX];          // plane n.y <= d (n = p_j - p_i, local coordinates)
+    double4 pl[T::PMAX];          // plane n.y <= d (n = p_j - p_i, local coordinates), exact
+    float4 fv[T::VMAX];           // FP32 copy of the vertex positions (x, y, z, 0)
     double vx[T::VMAX], vy[T::VMAX], vz[T::VMAX];
     uint32_t vt[T::VMAX];         // triplet a | b << 10 | c << 20, CCW seen from outside
     int32_t pid[T::PMAX];         // >= 0 Morton index of the neighbour site; -1-k box wall k
-    float4 qlo[T::QMAX];          // priority queue: the pushed child records (lo, maxw), (hi, link)
-    float4 qhi[T::QMAX];
+    union {
+        struct {                  // traversal: priority queue of pushed child records
+            float4 qlo[T::QMAX];  // (lo, maxw)
+            float4 qhi[T::QMAX];  // (hi, link)
+        };
+        struct {                  // finalize (the queue is dead by then)
+            uint16_t tw[3][T::VMAX];  // twin vertex across edges a->b, b->c, c->a
+            int32_t nb_id[T::PMAX];   // neighbour staging
+            float nb_area[T::PMAX];
+        };
+    };
     uint16_t rem[T::VMAX];        // removed-vertex slots of the current clip
     uint32_t omask[T::VC];        // outside-vertex ballots of the current clip
     uint32_t qmask[T::QC];        // alive-entry ballots of the current pop
     uint32_t bnd[T::VMAX + 64];   // boundary edges (x | y << 16) of the current clip
-    uint16_t tw[3][T::VMAX];      // finalize: twin vertex across edges a->b, b->c, c->a
     uint16_t pmap[T::PMAX];       // plane GC remap
-    int32_t nb_id[T::PMAX];       // finalize: neighbour staging
-    float nb_area[T::PMAX];
+    uint32_t ebits[T::EBW];       // hole-edge parity bitmap (zero between clips)
 };
 
 __device__ __forceinline__ int ford(float f) {
@@ -84,23 +107,32 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
-__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(FULL, v, src); }
-__device__ __forceinline__ float4 shfl_f4(float4 v, int src) {
-    return make_float4(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src), __shfl_sync(FULL, v.z, src),
-                       __shfl_sync(FULL, v.w, src));
+// Global-space atomics (the generic atomicAdd emits a shared/global runtime dispatch).
+__device__ __forceinline__ void red_add_g(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// Exact node tests switch on once a cell has visited this many nodes (heavy cells), or always with
-// PD_EXACT_NODES; PD_NO_EXACT disables them.
-constexpr unsigned long long kExactAfterNodes = 64;
-__device__ __forceinline__ bool exact_on(unsigned flags, unsigned long long visited) {
-    if (flags & PD_NO_EXACT) return false;
-    return (flags & PD_EXACT_NODES) || visited > kExactAfterNodes;
+__device__ __forceinline__ unsigned long long atom_add_g(unsigned long long* p, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ int atom_add_g32(int* p, int v) {
+    int old;
+    asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
     return v;
+}
+
+// Exact node tests switch on once a cell has visited `after` nodes (heavy cells), or always with
+// PD_EXACT_NODES; PD_NO_EXACT disables them.
+__device__ __forceinline__ bool exact_on(unsigned flags, unsigned long long visited, int after) {
+    if (flags & PD_NO_EXACT) return false;
+    return (flags & PD_EXACT_NODES) || visited > (unsigned long long)after;
 }
 
 enum { ST_OK = 0, ST_EMPTY = 1, ST_OVERFLOW = 2, ST_DUP = 3 };
@@ -115,10 +147,18 @@ struct Cell {
     double px, py, pz, pw;  // site (world), weight
     float fpx, fpy, fpz, fpw;
     float flo[3], fhi[3];   // cell AABB, site-local, rounded outward
+    float vmax;             // max_k max(|lo_k|, |hi_k|)
     float rmax;             // max corner distance of the AABB (isotropic radius bound)
     int nv, np, nq;
     int self;               // Morton index
     int self_orig;
+};
+
+// An FP32 plane with its certification margin: |s32 - s| <= err < m for s = n.v - d evaluated in
+// FP32 from the FP32 copies (all inputs carry <= 2^-24 relative rounding; the FMA chain adds a few
+// more).  m = 1e-6 (|n|_1 vmax + |D|^2 + |w_i - w_j|) is > 8x the worst-case error.
+struct FPlane {
+    float nx, ny, nz, d, m;
 };
 
 // r^2 of the directional radius for an octant set (one corner per octant is
@@ -165,22 +205,42 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
         float h1 = fmaxf(fmaxf(c.flo[1] * a1, c.flo[1] * b1), fmaxf(c.fhi[1] * a1, c.fhi[1] * b1));
         float h2 = fmaxf(fmaxf(c.flo[2] * a2, c.flo[2] * b2), fmaxf(c.fhi[2] * a2, c.fhi[2] * b2));
         float H = h0 + h1 + h2;
-        float mag = fmaxf(fabsf(c.flo[0]), c.fhi[0]) * fmaxf(fabsf(a0), fabsf(b0)) +
-                    fmaxf(fabsf(c.flo[1]), c.fhi[1]) * fmaxf(fabsf(a1), fabsf(b1)) +
-                    fmaxf(fabsf(c.flo[2]), c.fhi[2]) * fmaxf(fabsf(a2), fabsf(b2));
+        float mag = c.vmax * (fmaxf(fabsf(a0), fabsf(b0)) + fmaxf(fabsf(a1), fabsf(b1)) + fmaxf(fabsf(a2), fabsf(b2)));
         culled |= d2 + dw - 2.f * H > 1e-5f * (d2 + fabsf(dw) + 2.f * mag);
     }
     return d2 + dwn - r2;
 }
 
+// Exact polytope-vs-box node test (not in the paper; strictly tighter than any AABB bound).  The
+// plane of p_j (D = p_j - p_i) cuts the cell iff some vertex v has v.D - |D|^2/2 > (w_i - w_j)/2.
+// Over all p_j in the box, D_k in [a_k, b_k] and w_j <= w_max, and
+//   max_{D in box} (v.D - |D|^2/2) = sum_k (v_k c_k - c_k^2/2),  c_k = clamp(v_k, a_k, b_k),
+// (a separable concave maximisation), so the node is culled iff for every vertex that sum is
+// <= (w_i - w_max)/2.  Lanes = vertices, FP32 with a 1e-5 relative margin (only keeps nodes).
 template <class T>
-__device__ __noinline__ void update_aabb(WarpState<T>& S, Cell& c, int lane) {
+__device__ __noinline__ bool node_exact_culled(const WarpState<T>& S, const Cell& c, int lane, float4 lo_w, float4 hi_l) {
+    const float a0 = lo_w.x - c.fpx, a1 = lo_w.y - c.fpy, a2 = lo_w.z - c.fpz;
+    const float b0 = hi_l.x - c.fpx, b1 = hi_l.y - c.fpy, b2 = hi_l.z - c.fpz;
+    float best = -INFINITY;
+    for (int s = lane; s < c.nv; s += 32) {
+        float4 v = S.fv[s];
+        float cx = fminf(fmaxf(v.x, a0), b0), cy = fminf(fmaxf(v.y, a1), b1), cz = fminf(fmaxf(v.z, a2), b2);
+        best = fmaxf(best, cx * (v.x - 0.5f * cx) + cy * (v.y - 0.5f * cy) + cz * (v.z - 0.5f * cz));
+    }
+    best = iford(__reduce_max_sync(FULL, ford(best)));
+    const float B0 = fmaxf(fabsf(a0), fabsf(b0)), B1 = fmaxf(fabsf(a1), fabsf(b1)), B2 = fmaxf(fabsf(a2), fabsf(b2));
+    const float mag = B0 * (c.vmax + B0) + B1 * (c.vmax + B1) + B2 * (c.vmax + B2) + fabsf(c.fpw) + fabsf(lo_w.w);
+    return best < 0.5f * (c.fpw - lo_w.w) - 1e-5f * mag;
+}
+
+template <class T>
+__device__ __noinline__ void update_aabb(const WarpState<T>& S, Cell& c, int lane) {
     float lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY;
     for (int s = lane; s < c.nv; s += 32) {
-        double x = S.vx[s], y = S.vy[s], z = S.vz[s];
-        lo0 = fminf(lo0, __double2float_rd(x)); hi0 = fmaxf(hi0, __double2float_ru(x));
-        lo1 = fminf(lo1, __double2float_rd(y)); hi1 = fmaxf(hi1, __double2float_ru(y));
-        lo2 = fminf(lo2, __double2float_rd(z)); hi2 = fmaxf(hi2, __double2float_ru(z));
+        float4 v = S.fv[s];
+        lo0 = fminf(lo0, v.x); hi0 = fmaxf(hi0, v.x);
+        lo1 = fminf(lo1, v.y); hi1 = fmaxf(hi1, v.y);
+        lo2 = fminf(lo2, v.z); hi2 = fmaxf(hi2, v.z);
     }
     c.flo[0] = iford(__reduce_min_sync(FULL, ford(lo0)));
     c.flo[1] = iford(__reduce_min_sync(FULL, ford(lo1)));
@@ -188,10 +248,22 @@ __device__ __noinline__ void update_aabb(WarpState<T>& S, Cell& c, int lane) {
     c.fhi[0] = iford(__reduce_max_sync(FULL, ford(hi0)));
     c.fhi[1] = iford(__reduce_max_sync(FULL, ford(hi1)));
     c.fhi[2] = iford(__reduce_max_sync(FULL, ford(hi2)));
-    float rm2 = 0.f;
+    float rm2 = 0.f, vm = 0.f;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) rm2 += fmaxf(c.flo[k] * c.flo[k], c.fhi[k] * c.fhi[k]);
+    for (int k = 0; k < 3; ++k) {
+        // the FP32 copies are rounded to nearest: widen by 2 ulp so the box contains the FP64 cell
+        c.flo[k] -= fabsf(c.flo[k]) * 2.4e-7f + 1e-30f;
+        c.fhi[k] += fabsf(c.fhi[k]) * 2.4e-7f + 1e-30f;
+        rm2 += fmaxf(c.flo[k] * c.flo[k], c.fhi[k] * c.fhi[k]);
+        vm = fmaxf(vm, fmaxf(-c.flo[k], c.fhi[k]));
+    }
     c.rmax = sqrtf(rm2);
+    c.vmax = vm;
+}
+
+__device__ __forceinline__ void put_vertex(float4* fv, double* vx, double* vy, double* vz, int s, double x, double y, double z) {
+    vx[s] = x; vy[s] = y; vz[s] = z;
+    fv[s] = make_float4((float)x, (float)y, (float)z, 0.f);
 }
 
 // Plane garbage collection: drop planes no vertex references.
@@ -238,10 +310,18 @@ __device__ __forceinline__ void solve3(double4 a, double4 b, double4 c, double& 
     z = (a.w * bcz + b.w * caz + c.w * abz) * inv;
 }
 
+// Is vertex s strictly outside the plane?  FP32 filter, FP64 certification within the margin.
+template <class T>
+__device__ __forceinline__ bool outside(const WarpState<T>& S, int s, const FPlane& f, const double4& pl, double tol) {
+    float4 v = S.fv[s];
+    float s32 = fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d;
+    if (fabsf(s32) > f.m) return s32 > 0.f;
+    return fma(pl.x, S.vx[s], fma(pl.y, S.vy[s], pl.z * S.vz[s])) - pl.w > tol;
+}
+
 // Clip the cell by {y : n.y <= d} (re-designed warp-parallel).
 template <class T>
-__device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double nx, double ny, double nz, double d,
-                                 double tol, int pidn) {
+__device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, double tol, FPlane f, int pidn) {
     if (c.np >= (T::PMAX * 85) / 100) {
         plane_gc(S, c, lane);
         if (c.np >= T::PMAX) return CLIP_OVF;
@@ -251,8 +331,7 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double nx, 
     const int nch = (c.nv + 31) >> 5;
     for (int ch = 0; ch < nch; ++ch) {
         int s = ch * 32 + lane;
-        bool out = false;
-        if (s < c.nv) out = fma(nx, S.vx[s], fma(ny, S.vy[s], nz * S.vz[s])) - d > tol;
+        bool out = s < c.nv && outside(S, s, f, pl, tol);
         unsigned m = __ballot_sync(FULL, out);
         if (out) S.rem[R + __popc(m & lanemask_lt())] = (uint16_t)s;  // removed slots, ascending
         if (lane == 0) S.omask[ch] = m;
@@ -262,28 +341,51 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double nx, 
     if (R == c.nv) return CLIP_EMPTY;
     __syncwarp();
     // 2. hole boundary: edge x->y of a removed vertex is a boundary edge iff its reverse y->x is not
-    //    held by another removed vertex.
+    //    held by another removed vertex.  Small tiers: each removed vertex toggles the parity bit of
+    //    its 3 unordered edges {x,y}; interior edges are toggled twice.  Large tiers: pairwise scan.
+    if (T::EDGE_BITMAP) {
+        for (int r = lane; r < R; r += 32) {
+            uint32_t t = S.vt[S.rem[r]];
+            int a = ta(t), b = tb(t), cc = tc(t);
+            int k0 = min(a, b) * T::PMAX + max(a, b), k1 = min(b, cc) * T::PMAX + max(b, cc),
+                k2 = min(cc, a) * T::PMAX + max(cc, a);
+            atomicXor(&S.ebits[k0 >> 5], 1u << (k0 & 31));
+            atomicXor(&S.ebits[k1 >> 5], 1u << (k1 & 31));
+            atomicXor(&S.ebits[k2 >> 5], 1u << (k2 & 31));
+        }
+        __syncwarp();
+    }
     int B = 0;
     for (int r0 = 0; r0 < R; r0 += 32) {
         int r = r0 + lane;
         int nb = 0;
-        uint32_t e[3];
+        uint32_t e0 = 0, e1 = 0, e2 = 0;
         if (r < R) {
             uint32_t t = S.vt[S.rem[r]];
             int a = ta(t), b = tb(t), cc = tc(t);
             bool f0 = false, f1 = false, f2 = false;
-            #pragma unroll 1
-            for (int k = 0; k < R; ++k) {
-                uint32_t u = S.vt[S.rem[k]];
-                f0 |= has_edge(u, b, a);
-                f1 |= has_edge(u, cc, b);
-                f2 |= has_edge(u, a, cc);
+            if (T::EDGE_BITMAP) {
+                int k0 = min(a, b) * T::PMAX + max(a, b), k1 = min(b, cc) * T::PMAX + max(b, cc),
+                    k2 = min(cc, a) * T::PMAX + max(cc, a);
+                f0 = !((S.ebits[k0 >> 5] >> (k0 & 31)) & 1u);
+                f1 = !((S.ebits[k1 >> 5] >> (k1 & 31)) & 1u);
+                f2 = !((S.ebits[k2 >> 5] >> (k2 & 31)) & 1u);
+            } else {
+#pragma unroll 1
+                for (int k = 0; k < R; ++k) {
+                    uint32_t u = S.vt[S.rem[k]];
+                    f0 |= has_edge(u, b, a);
+                    f1 |= has_edge(u, cc, b);
+                    f2 |= has_edge(u, a, cc);
+                }
             }
-            if (!f0) e[nb++] = (uint32_t)a | ((uint32_t)b << 16);
-            if (!f1) e[nb++] = (uint32_t)b | ((uint32_t)cc << 16);
-            if (!f2) e[nb++] = (uint32_t)cc | ((uint32_t)a << 16);
+            // compact the (up to 3) boundary edges without local-memory arrays
+            uint32_t ab = (uint32_t)a | ((uint32_t)b << 16), bc = (uint32_t)b | ((uint32_t)cc << 16),
+                     ca = (uint32_t)cc | ((uint32_t)a << 16);
+            if (!f0) { e0 = ab; nb = 1; }
+            if (!f1) { if (nb == 0) e0 = bc; else e1 = bc; nb++; }
+            if (!f2) { if (nb == 0) e0 = ca; else if (nb == 1) e1 = ca; else e2 = ca; nb++; }
         }
-        // inclusive scan of nb
         int inc = nb;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -293,29 +395,41 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double nx, 
         int tot = __shfl_sync(FULL, inc, 31);
         int pos = B + inc - nb;
         if (B + tot <= T::VMAX + 64) {
-            for (int k = 0; k < nb; ++k) S.bnd[pos + k] = e[k];
+            if (nb > 0) S.bnd[pos] = e0;
+            if (nb > 1) S.bnd[pos + 1] = e1;
+            if (nb > 2) S.bnd[pos + 2] = e2;
         }
         B += tot;
+    }
+    if (T::EDGE_BITMAP) {  // restore the all-zero bitmap
+        __syncwarp();
+        for (int r = lane; r < R; r += 32) {
+            uint32_t t = S.vt[S.rem[r]];
+            int a = ta(t), b = tb(t), cc = tc(t);
+            S.ebits[(min(a, b) * T::PMAX + max(a, b)) >> 5] = 0u;
+            S.ebits[(min(b, cc) * T::PMAX + max(b, cc)) >> 5] = 0u;
+            S.ebits[(min(cc, a) * T::PMAX + max(cc, a)) >> 5] = 0u;
+        }
+        __syncwarp();
     }
     int nvn = c.nv - R + B;
     if (nvn > T::VMAX || B > T::VMAX + 64 || c.np + 1 > T::PMAX) return CLIP_OVF;
     // 3. append the plane, create (h, x, y) for every boundary edge
     int hs = c.np;
     if (lane == 0) {
-        S.pl[hs] = make_double4(nx, ny, nz, d);
+        S.pl[hs] = pl;
         S.pid[hs] = pidn;
     }
     __syncwarp();
-    double4 ph = make_double4(nx, ny, nz, d);
     for (int e0 = 0; e0 < B; e0 += 32) {
         int e = e0 + lane;
         if (e < B) {
             uint32_t be = S.bnd[e];
             int x = be & 0xffff, y = be >> 16;
             double vx, vy, vz;
-            solve3(ph, S.pl[x], S.pl[y], vx, vy, vz);
+            solve3(pl, S.pl[x], S.pl[y], vx, vy, vz);
             int slot = e < R ? S.rem[e] : c.nv + (e - R);
-            S.vx[slot] = vx; S.vy[slot] = vy; S.vz[slot] = vz;
+            put_vertex(S.fv, S.vx, S.vy, S.vz, slot, vx, vy, vz);
             S.vt[slot] = tpack(hs, x, y);
         }
     }
@@ -329,6 +443,7 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double nx, 
             if (mover) {
                 int dst = S.rem[B + moved + __popc(mm & lanemask_lt())];
                 S.vx[dst] = S.vx[s]; S.vy[dst] = S.vy[s]; S.vz[dst] = S.vz[s];
+                S.fv[dst] = S.fv[s];
                 S.vt[dst] = S.vt[s];
             }
             moved += __popc(mm);
@@ -341,113 +456,105 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double nx, 
     return CLIP_DONE;
 }
 
-// Site test in FP64: cull iff the plane y.D <= q/2 (q = |D|^2 + w_i - w_j)
-// cannot cut the cell.  Paper: d_ij = q/(2|D|) > r with r the directional radius of p_j's octant,
-// i.e. q > 0 and q^2 > 4 r^2 |D|^2.  Default: the exact support of the cell AABB in direction D,
-// h = sum_k max(lo_k D_k, hi_k D_k) <= r |D| (Cauchy-Schwarz), cull iff q/2 > h: never looser.
-__device__ __forceinline__ bool site_culled(const Cell& c, double Dx, double Dy, double Dz, double q, double D2,
+// Site test in FP32: cull iff the plane y.D <= q/2 (q = |D|^2 + w_i - w_j)
+// cannot cut the cell.  Paper: d_ij = q/(2|D|) > r with r the directional radius of p_j's octant.
+// Default: the exact support of the cell AABB in direction D, h = sum_k max(lo_k D_k, hi_k D_k)
+// <= r |D| (Cauchy-Schwarz), cull iff q/2 > h: never looser.  Margins only ever keep a site.
+__device__ __forceinline__ bool site_culled(const Cell& c, float Dx, float Dy, float Dz, float D2, float dq,
                                             unsigned flags) {
+    const float q = D2 + dq;
     if (!(flags & (PD_PAPER_BOUND | PD_ISOTROPIC))) {
-        double h = Dx * (Dx >= 0 ? (double)c.fhi[0] : (double)c.flo[0]) + Dy * (Dy >= 0 ? (double)c.fhi[1] : (double)c.flo[1]) +
-                   Dz * (Dz >= 0 ? (double)c.fhi[2] : (double)c.flo[2]);
-        return 0.5 * q > h + 1e-9 * (fabs(h) + D2);
+        float h = Dx * (Dx >= 0.f ? c.fhi[0] : c.flo[0]) + Dy * (Dy >= 0.f ? c.fhi[1] : c.flo[1]) +
+                  Dz * (Dz >= 0.f ? c.fhi[2] : c.flo[2]);
+        float mag = c.vmax * (fabsf(Dx) + fabsf(Dy) + fabsf(Dz));
+        return 0.5f * q - h > 1e-5f * (D2 + fabsf(dq) + mag);
     }
-    double r2;
+    float r2;
     if (flags & PD_ISOTROPIC) {
-        r2 = 0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) r2 += (double)fmaxf(c.flo[k] * c.flo[k], c.fhi[k] * c.fhi[k]);
+        r2 = c.rmax * c.rmax;
     } else {
-        double hx = Dx >= 0 ? c.fhi[0] : c.flo[0], hy = Dy >= 0 ? c.fhi[1] : c.flo[1], hz = Dz >= 0 ? c.fhi[2] : c.flo[2];
+        float hx = Dx >= 0.f ? c.fhi[0] : c.flo[0], hy = Dy >= 0.f ? c.fhi[1] : c.flo[1], hz = Dz >= 0.f ? c.fhi[2] : c.flo[2];
         r2 = hx * hx + hy * hy + hz * hz;
     }
-    return q > 0 && q * q > 4.0 * r2 * D2 * (1.0 + 1e-9);
-}
-
-// Exact polytope-vs-box node test (not in the paper; strictly tighter than any AABB bound).  The
-// plane of p_j (D = p_j - p_i) cuts the cell iff some vertex v has v.D - |D|^2/2 > (w_i - w_j)/2.
-// Over all p_j in the box, D_k in [a_k, b_k] and w_j <= w_max, and
-//   max_{D in box} (v.D - |D|^2/2) = sum_k (v_k c_k - c_k^2/2),  c_k = clamp(v_k, a_k, b_k),
-// (a separable concave maximisation), so the node is culled iff for every vertex that sum is
-// <= (w_i - w_max)/2.  Lanes = vertices, FP64, relative margin so rounding only keeps nodes.
-template <class T>
-__device__ __noinline__ bool node_exact_culled(const WarpState<T>& S, const Cell& c, int lane, float4 lo_w, float4 hi_l) {
-    const double a0 = (double)lo_w.x - c.px, a1 = (double)lo_w.y - c.py, a2 = (double)lo_w.z - c.pz;
-    const double b0 = (double)hi_l.x - c.px, b1 = (double)hi_l.y - c.py, b2 = (double)hi_l.z - c.pz;
-    const double rhs = 0.5 * (c.pw - (double)lo_w.w);
-    double best = -1e300, mag = 0.0;
-    for (int s = lane; s < c.nv; s += 32) {
-        double vx = S.vx[s], vy = S.vy[s], vz = S.vz[s];
-        double cx = fmin(fmax(vx, a0), b0), cy = fmin(fmax(vy, a1), b1), cz = fmin(fmax(vz, a2), b2);
-        double f = cx * (vx - 0.5 * cx) + cy * (vy - 0.5 * cy) + cz * (vz - 0.5 * cz);
-        best = fmax(best, f);
-        mag = fmax(mag, fabs(cx * vx) + fabs(cy * vy) + fabs(cz * vz));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        best = fmax(best, __shfl_xor_sync(FULL, best, o));
-        mag = fmax(mag, __shfl_xor_sync(FULL, mag, o));
-    }
-    return best < rhs - 1e-12 * (mag + fabs(rhs));
+    float rd = sqrtf(r2 * D2);
+    return q - 2.f * rd > 1e-5f * (D2 + fabsf(dq) + 2.f * rd);
 }
 
 template <class T>
 __device__ __noinline__ int process_leaf(WarpState<T>& S, Cell& c, int lane, int link, const CellParams& P, Counters& cnt) {
-    int first = leaf_first(link), count = leaf_count(link);
-    int j = first + lane;
+    const int first = leaf_first(link), count = leaf_count(link);
+    const int j = first + lane;
     bool valid = lane < count && j != c.self;
-    double Dx = 0, Dy = 0, Dz = 0, q = 0, D2 = 0;
-    float wj = 0.f;
+    float4 sj = make_float4(0.f, 0.f, 0.f, 0.f);
+    float Dx = 0.f, Dy = 0.f, Dz = 0.f, D2 = 0.f, dq = 0.f;
     bool dup_kill = false;
     if (valid) {
-        float4 s = __ldg(&P.sites[j]);
-        wj = s.w;
-        Dx = (double)s.x - c.px; Dy = (double)s.y - c.py; Dz = (double)s.z - c.pz;
+        sj = __ldg(&P.sites[j]);
+        Dx = sj.x - c.fpx; Dy = sj.y - c.fpy; Dz = sj.z - c.fpz;  // exact iff zero: duplicates are detected exactly
         D2 = Dx * Dx + Dy * Dy + Dz * Dz;
-        q = D2 + (c.pw - (double)s.w);
-        if (D2 == 0.0) {
+        dq = c.fpw - sj.w;
+        if (Dx == 0.f && Dy == 0.f && Dz == 0.f) {
             // coincident sites: the heavier owns, ties to the lower id
-            if (s.w > c.fpw || (s.w == c.fpw && __ldg(&P.perm[j]) < c.self_orig)) dup_kill = true;
+            if (sj.w > c.fpw || (sj.w == c.fpw && __ldg(&P.perm[j]) < c.self_orig)) dup_kill = true;
             valid = false;
         }
     }
     if (__any_sync(FULL, dup_kill)) return ST_DUP;
-    cnt.sites += __popc(__ballot_sync(FULL, lane < count));
-    bool cand = valid && !site_culled(c, Dx, Dy, Dz, q, D2, P.flags);
+    cnt.sites += count;
+    bool cand = valid && !site_culled(c, Dx, Dy, Dz, D2, dq, P.flags);
     unsigned mask = __ballot_sync(FULL, cand);
     if (!mask) return ST_OK;
     // Batch cut test, lane = candidate: does the plane cut the CURRENT cell?  A plane that does not
-    // cut it cannot cut any later (smaller) cell, so it is dropped for good.  Same FP64 predicate
-    // as clip().
-    const float nD = sqrtf((float)D2);
-    const double tol = 1e-12 * (double)nD * (double)c.rmax;
-    const double dd = 0.5 * q;
+    // cut it cannot cut any later (smaller) cell, so it is dropped for good.  Same certified
+    // predicate as clip().
+    const float dd = 0.5f * (D2 + dq);
+    const float m = 1e-6f * ((fabsf(Dx) + fabsf(Dy) + fabsf(Dz)) * c.vmax + D2 + fabsf(dq));
     {
-        bool cuts = false;
-#pragma unroll 2
-        for (int k = 0; k < c.nv; ++k) {
-            double s = fma(Dx, S.vx[k], fma(Dy, S.vy[k], Dz * S.vz[k])) - dd;
-            cuts |= s > tol;
+        bool cuts = false, amb = false;
+        if (cand) {
+#pragma unroll 4
+            for (int k = 0; k < c.nv; ++k) {
+                float4 v = S.fv[k];
+                float s = fmaf(Dx, v.x, fmaf(Dy, v.y, Dz * v.z)) - dd;
+                cuts |= s > m;
+                amb |= fabsf(s) <= m;
+            }
+            if (!cuts && amb) {  // certify in FP64 (rare)
+                double ex = (double)sj.x - c.px, ey = (double)sj.y - c.py, ez = (double)sj.z - c.pz;
+                double ed = 0.5 * (ex * ex + ey * ey + ez * ez + (c.pw - (double)sj.w));
+                double tol = 1e-12 * (double)sqrtf(D2) * (double)c.rmax;
+                for (int k = 0; k < c.nv && !cuts; ++k)
+                    cuts = fma(ex, S.vx[k], fma(ey, S.vy[k], ez * S.vz[k])) - ed > tol;
+            }
         }
         cnt.tests += __popc(mask);
         cand = cand && cuts;
         mask = __ballot_sync(FULL, cand);
     }
-    float key = cand ? (float)(q / (double)nD) : INFINITY;  // 2 d_ij: nearest plane first
+    float key = cand ? dd * rsqrtf(D2) : INFINITY;  // d_ij: nearest plane first
     while (mask) {
         int kmin = __reduce_min_sync(FULL, cand ? ford(key) : 0x7fffffff);
         unsigned lead = __ballot_sync(FULL, cand && ford(key) == kmin);
         int src = __ffs(lead) - 1;
-        double nx = shfl_d(Dx, src), ny = shfl_d(Dy, src), nz = shfl_d(Dz, src), qq = shfl_d(dd, src);
-        double tt = shfl_d(tol, src);
-        int jj = __shfl_sync(FULL, j, src);
+        float sx = __shfl_sync(FULL, sj.x, src), sy = __shfl_sync(FULL, sj.y, src), sz = __shfl_sync(FULL, sj.z, src),
+              sw = __shfl_sync(FULL, sj.w, src);
         if (lane == src) cand = false;
-        int st = clip(S, c, lane, nx, ny, nz, qq, tt, jj);
+        // the exact plane of the selected candidate, recomputed identically on every lane
+        double ex = (double)sx - c.px, ey = (double)sy - c.py, ez = (double)sz - c.pz;
+        double e2 = ex * ex + ey * ey + ez * ez;
+        double4 pl = make_double4(ex, ey, ez, 0.5 * (e2 + (c.pw - (double)sw)));
+        double tol = 1e-12 * (double)sqrtf((float)e2) * (double)c.rmax;
+        FPlane f;
+        f.nx = sx - c.fpx; f.ny = sy - c.fpy; f.nz = sz - c.fpz;
+        float f2 = f.nx * f.nx + f.ny * f.ny + f.nz * f.nz, fdq = c.fpw - sw;
+        f.d = 0.5f * (f2 + fdq);
+        f.m = 1e-6f * ((fabsf(f.nx) + fabsf(f.ny) + fabsf(f.nz)) * c.vmax + f2 + fabsf(fdq));
+        int st = clip(S, c, lane, pl, tol, f, first + src);
         if (st == CLIP_EMPTY) return ST_EMPTY;
         if (st == CLIP_OVF) return ST_OVERFLOW;
         if (st == CLIP_DONE) {
             cnt.clips++;
-            if (cand && site_culled(c, Dx, Dy, Dz, q, D2, P.flags)) cand = false;
+            if (cand && site_culled(c, Dx, Dy, Dz, D2, dq, P.flags)) cand = false;
         }
         mask = __ballot_sync(FULL, cand);
     }
@@ -468,41 +575,52 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
     c.nq = 0;
     for (;;) {
         if (have) {
-            while (node >= 0) {  // descend (Alg. 1 lines 4-18)
+            while (node >= 0) {  // descend (Alg. 1 lines 4-18), 8 children per visit
                 cnt.nodes++;
                 float key = INFINITY;
                 bool culled = true;
                 float4 lo_w = make_float4(0, 0, 0, 0), hi_l = make_float4(0, 0, 0, 0);
-                if (lane < 2) {
-                    const NodeChild* ch = &P.nodes[node].c[lane];
-                    lo_w = __ldg(&ch->lo_w);
-                    hi_l = __ldg(&ch->hi_l);
-                    key = node_test(c, lo_w, hi_l, P.flags, culled);
+                const NodeChild* rec = P.nodes[node].c;
+                if (lane < WIDE) {
+                    lo_w = __ldg(&rec[lane].lo_w);
+                    hi_l = __ldg(&rec[lane].hi_l);
+                    if (__float_as_int(hi_l.w) != EMPTY_LINK) key = node_test(c, lo_w, hi_l, P.flags, culled);
                 }
-                bool c0 = __shfl_sync(FULL, culled, 0), c1 = __shfl_sync(FULL, culled, 1);
-                if (exact_on(P.flags, cnt.nodes - nodes0)) {
-                    float4 l0 = shfl_f4(lo_w, 0), h0 = shfl_f4(hi_l, 0), l1 = shfl_f4(lo_w, 1), h1 = shfl_f4(hi_l, 1);
-                    if (!c0) c0 = node_exact_culled(S, c, lane, l0, h0);
-                    if (!c1) c1 = node_exact_culled(S, c, lane, l1, h1);
-                    if (lane == 0) culled = c0;
-                    if (lane == 1) culled = c1;
-                }
-                if (c0 && c1) { have = false; break; }
-                float k0 = __shfl_sync(FULL, key, 0), k1 = __shfl_sync(FULL, key, 1);
-                int near = (!c0 && (c1 || k0 <= k1)) ? 0 : 1;
-                int far = 1 - near;
-                bool cfar = far ? c1 : c0;
-                int lnear = __shfl_sync(FULL, __float_as_int(hi_l.w), near);
-                if (!cfar) {
-                    if (c.nq < T::QMAX) {
-                        if (lane == far) { S.qlo[c.nq] = lo_w; S.qhi[c.nq] = hi_l; }
-                        c.nq++;
-                    } else {
-                        if (ns >= spill_cap) return ST_OVERFLOW;
-                        if (lane == far) { spill[ns].lo_w = lo_w; spill[ns].hi_l = hi_l; }
-                        ns++;
-                        cnt.spills++;
+                unsigned surv = __ballot_sync(FULL, !culled);
+                if (surv && exact_on(P.flags, cnt.nodes - nodes0, P.exact_after)) {
+                    unsigned s2 = surv;
+                    while (s2) {
+                        int k = __ffs(s2) - 1;
+                        s2 &= s2 - 1;
+                        if (node_exact_culled(S, c, lane, __ldg(&rec[k].lo_w), __ldg(&rec[k].hi_l))) surv &= ~(1u << k);
                     }
+                    culled = !((surv >> lane) & 1u);
+                }
+                if (!surv) { have = false; break; }
+                // go to the child with the smallest priority delta, queue the other survivors
+                int kmin = __reduce_min_sync(FULL, culled ? 0x7fffffff : ford(key));
+                int near = __ffs(__ballot_sync(FULL, !culled && ford(key) == kmin)) - 1;
+                int lnear = __shfl_sync(FULL, __float_as_int(hi_l.w), near);
+                bool push = !culled && lane != near;
+                unsigned pm = __ballot_sync(FULL, push);
+                int npush = __popc(pm);
+                if (npush) {
+                    int rank = __popc(pm & lanemask_lt());
+                    int room = T::QMAX - c.nq;
+                    int tos = max(npush - room, 0);
+                    if (ns + tos > spill_cap) return ST_OVERFLOW;
+                    if (push) {
+                        if (rank < room) {
+                            S.qlo[c.nq + rank] = lo_w;
+                            S.qhi[c.nq + rank] = hi_l;
+                        } else {
+                            spill[ns + rank - room].lo_w = lo_w;
+                            spill[ns + rank - room].hi_l = hi_l;
+                        }
+                    }
+                    c.nq += npush - tos;
+                    ns += tos;
+                    cnt.spills += tos;
                 }
                 node = lnear;
             }
@@ -517,14 +635,14 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         __syncwarp();
         if (c.nq == 0 && ns > 0) {  // refill from the spill stack
             __threadfence_block();
-            int m = min(ns, T::QMAX);
-            for (int t = lane; t < m; t += 32) {
-                NodeChild e = spill[ns - m + t];
+            int mm = min(ns, T::QMAX);
+            for (int t = lane; t < mm; t += 32) {
+                NodeChild e = spill[ns - mm + t];
                 S.qlo[t] = e.lo_w;
                 S.qhi[t] = e.hi_l;
             }
-            ns -= m;
-            c.nq = m;
+            ns -= mm;
+            c.nq = mm;
             __syncwarp();
         }
         if (c.nq == 0) return ST_OK;
@@ -571,7 +689,8 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         unsigned lead = __ballot_sync(FULL, bestk == gk);
         int bslot = __shfl_sync(FULL, bests, __ffs(lead) - 1);
         node = __float_as_int(S.qhi[bslot].w);
-        bool popped_dead = exact_on(P.flags, cnt.nodes - nodes0) && node_exact_culled(S, c, lane, S.qlo[bslot], S.qhi[bslot]);
+        bool popped_dead = exact_on(P.flags, cnt.nodes - nodes0, P.exact_after) &&
+                           node_exact_culled(S, c, lane, S.qlo[bslot], S.qhi[bslot]);
         // compact: keep alive entries except the popped one
         int base = 0;
         for (int ch = 0; ch < qch; ++ch) {
@@ -608,27 +727,19 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
     }
     if (lane < 8) {
         int sx = lane & 1, sy = (lane >> 1) & 1, sz = (lane >> 2) & 1;
-        S.vx[lane] = sx ? hi[0] : lo[0];
-        S.vy[lane] = sy ? hi[1] : lo[1];
-        S.vz[lane] = sz ? hi[2] : lo[2];
+        put_vertex(S.fv, S.vx, S.vy, S.vz, lane, sx ? hi[0] : lo[0], sy ? hi[1] : lo[1], sz ? hi[2] : lo[2]);
         int X = sx, Y = 2 + sy, Z = 4 + sz;
         int sgn = (sx ? 1 : -1) * (sy ? 1 : -1) * (sz ? 1 : -1);  // det of the outward normals
         S.vt[lane] = sgn > 0 ? tpack(X, Y, Z) : tpack(X, Z, Y);
     }
-    float rm2 = 0.f;
-    for (int k = 0; k < 3; ++k) {
-        c.flo[k] = __double2float_rd(lo[k]);
-        c.fhi[k] = __double2float_ru(hi[k]);
-        rm2 += fmaxf(c.flo[k] * c.flo[k], c.fhi[k] * c.fhi[k]);
-    }
-    c.rmax = sqrtf(rm2);
     c.nv = 8;
     c.np = 6;
     c.nq = 0;
     __syncwarp();
+    update_aabb(S, c, lane);
 }
 
-// Face areas (vector area 1/2 sum v x next(v) around each face), volume, neighbours.
+// Face areas (vector area 1/2 sum v x next(v) around each face), volume, neighbours; FP64.
 template <class T>
 __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const CellParams& P, int status) {
     const int i = c.self_orig;
@@ -649,7 +760,7 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
         uint32_t t = S.vt[u];
         int a = ta(t), b = tb(t), cc = tc(t);
         uint16_t t0 = 0xffff, t1 = 0xffff, t2 = 0xffff;
-        #pragma unroll 1
+#pragma unroll 1
         for (int k = 0; k < c.nv; ++k) {
             uint32_t w = S.vt[k];
             if (has_edge(w, b, a)) t0 = (uint16_t)k;
@@ -666,7 +777,7 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
         int f = f0 + lane;
         double Ax = 0, Ay = 0, Az = 0;
         if (f < c.np) {
-            #pragma unroll 1
+#pragma unroll 1
             for (int u = 0; u < c.nv; ++u) {
                 uint32_t t = S.vt[u];
                 int which = ta(t) == f ? 2 : (tb(t) == f ? 0 : (tc(t) == f ? 1 : -1));
@@ -707,14 +818,14 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
     __syncwarp();
     // arena row (ascending original ids)
     long long base = 0;
-    if (lane == 0) base = (long long)atomicAdd(O.arena_top, (unsigned long long)K);
+    if (lane == 0) base = (long long)atom_add_g(O.arena_top, (unsigned long long)K);
     base = __shfl_sync(FULL, base, 0);
     bool fits = base + K <= O.arena_cap;
     if (fits) {
         for (int e = lane; e < K; e += 32) {
             int id = S.nb_id[e];
             int rank = 0;
-            #pragma unroll 1
+#pragma unroll 1
             for (int k = 0; k < K; ++k) rank += S.nb_id[k] < id;
             O.arena_nbr[base + rank] = id;
             O.arena_area[base + rank] = S.nb_area[e];
@@ -732,7 +843,7 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
 }
 
 template <class T>
-__global__ void __launch_bounds__(T::WARPS * 32) cells_kernel(CellParams P, int tier) {
+__global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(CellParams P, int tier) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpState<T>& S = reinterpret_cast<WarpState<T>*>(smem_raw)[wid];
@@ -740,11 +851,13 @@ __global__ void __launch_bounds__(T::WARPS * 32) cells_kernel(CellParams P, int 
     Counters cnt = {0, 0, 0, 0, 0, 0};
     const int gw = blockIdx.x * T::WARPS + wid;
     NodeChild* spill = P.spill + (size_t)gw * P.spill_cap;
+    for (int k = lane; k < T::EBW; k += 32) S.ebits[k] = 0u;
+    __syncwarp();
     unsigned long long ncells = 0, novf = 0;
     constexpr int BATCH = 4;
     for (;;) {
         long long b0 = 0;
-        if (lane == 0) b0 = (long long)atomicAdd(P.work_counter, (unsigned long long)BATCH);
+        if (lane == 0) b0 = (long long)atom_add_g(P.work_counter, (unsigned long long)BATCH);
         b0 = __shfl_sync(FULL, b0, 0);
         if (b0 >= total) break;
         for (int b = 0; b < BATCH && b0 + b < total; ++b) {
@@ -762,7 +875,7 @@ __global__ void __launch_bounds__(T::WARPS * 32) cells_kernel(CellParams P, int 
             __syncwarp();
             if (st == ST_OVERFLOW && !P.last_tier) {
                 if (lane == 0) {
-                    int k = atomicAdd(P.next_count, 1);
+                    int k = atom_add_g32(P.next_count, 1);
                     P.next_list[k] = s;
                 }
                 continue;
@@ -778,15 +891,15 @@ __global__ void __launch_bounds__(T::WARPS * 32) cells_kernel(CellParams P, int 
         }
     }
     if ((P.flags & PD_STATS) && lane == 0) {
-        atomicAdd(&P.stats->nodes, cnt.nodes);
-        atomicAdd(&P.stats->leaves, cnt.leaves);
-        atomicAdd(&P.stats->sites, cnt.sites);
-        atomicAdd(&P.stats->clip_tests, cnt.tests);
-        atomicAdd(&P.stats->clips, cnt.clips);
-        atomicAdd(&P.stats->cells, ncells);
-        atomicAdd(&P.stats->tier[tier], ncells);
-        atomicAdd(&P.stats->overflow, novf);
-        atomicAdd(&P.stats->spills, cnt.spills);
+        red_add_g(&P.stats->nodes, cnt.nodes);
+        red_add_g(&P.stats->leaves, cnt.leaves);
+        red_add_g(&P.stats->sites, cnt.sites);
+        red_add_g(&P.stats->clip_tests, cnt.tests);
+        red_add_g(&P.stats->clips, cnt.clips);
+        red_add_g(&P.stats->cells, ncells);
+        red_add_g(&P.stats->tier[tier], ncells);
+        red_add_g(&P.stats->overflow, novf);
+        red_add_g(&P.stats->spills, cnt.spills);
     }
 }
 

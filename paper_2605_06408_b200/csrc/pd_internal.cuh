@@ -15,8 +15,12 @@ struct __align__(16) NodeChild {
     float4 lo_w;
     float4 hi_l;
 };
-struct __align__(64) NodeRec {
-    NodeChild c[2];
+// 8-wide BVH node (the binary LBVH collapsed top-down): lane k of a warp reads child k, so one node
+// visit is a single coalesced 256-byte read and 8 parallel child tests.
+constexpr int WIDE = 8;
+constexpr int EMPTY_LINK = 0x7fffffff;  // unused child slot
+struct __align__(256) WideNode {
+    NodeChild c[WIDE];
 };
 
 __host__ __device__ inline int leaf_link(int first, int count) { return ~((first << 5) | (count - 1)); }
@@ -24,9 +28,10 @@ __host__ __device__ inline int leaf_first(int link) { return (~link) >> 5; }
 __host__ __device__ inline int leaf_count(int link) { return ((~link) & 31) + 1; }
 
 struct Bvh {
-    NodeRec* nodes = nullptr;   // n-1 internal nodes (Karras order); unused when n <= leaf
+    WideNode* nodes = nullptr;  // wide nodes (<= 2n/l + 2); unused when n <= leaf
     NodeChild* root = nullptr;  // device: 1 record describing the root (bounds + link)
-    int n_internal = 0;
+    int n_wide = 0;
+    int levels = 0;
 };
 
 // Per-cell outputs of the cell kernel, indexed by ORIGINAL id (cells outside a shard untouched).
@@ -51,7 +56,7 @@ struct Stats {  // device counters (PD_STATS)
 struct CellParams {
     const float4* sites;  // Morton-sorted (x, y, z, w)
     const int32_t* perm;  // Morton position -> original id
-    const NodeRec* nodes;
+    const WideNode* nodes;
     const NodeChild* root;
     float box_lo[3], box_hi[3];
     unsigned flags;
@@ -69,6 +74,7 @@ struct CellParams {
     Stats* stats;
     NodeChild* spill;   // per-warp queue spill stacks (global memory)
     int spill_cap;      // entries per warp
+    int exact_after;    // exact node tests once a cell has visited this many nodes
 };
 
 cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches);
