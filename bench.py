@@ -264,7 +264,7 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
                 "config": {"workload": f"{wl.name}: {wl.description}", "n": wl.n, "box": list(wl.box),
-                           "leaf_size": args.leaf or 16, "parallelism": f"seed-sharded x{world}",
+                           "leaf_size": args.leaf or 32, "parallelism": f"seed-sharded x{world}",
                            "l2": "flushed before every timed step (256 MiB write)", "generation_s": round(gen_s, 1)},
                 "roofline": roof,
                 "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},

@@ -27,7 +27,9 @@
  *      the `order_k` nearest sites are clipped first (ascending |D|), then every site in index
  *      order.  order_k = 0 gives plain index order (tests check both agree).
  *   3. Face area by Newell's formula, vol = 1/3 sum_f A_f . c_f, S_i = sum of all face areas
- *      (walls included); neighbours = bisector faces with area > 0, ascending.
+ *      (walls included); neighbours = bisector faces with area > 1e-13 S_i, ascending (a smaller
+ *      "area" is the FP64 rounding residue of a zero-area edge/vertex contact of a degenerate,
+ *      e.g. cospherical, configuration: DESIGN.md reading R2 / SURVEY.md §8(c) Q2).
  *   Coincident sites (bit-identical FP32 positions): the heavier owns, ties go
  *   to the lower id; the other cell is EMPTY|DUPLICATE (Eq. 1: its cell is the empty set).
  *
@@ -363,8 +365,12 @@ static void finalize_cell(const poly_t* p, orc_cell* out, int flags) {
         surf += area;
         out->tags[f] = F->tag;
         out->areas[f] = area;
-        if (F->tag < 0) { if (area > 0) out->flags |= ORC_BOUNDARY; }
-        else if (area > 0) { ta[2 * nt] = (double)F->tag; ta[2 * nt + 1] = area; nt++; }
+    }
+    double amin = 1e-13 * surf;   /* zero-area contacts: reading R2 */
+    for (int f = 0; f < p->nf; ++f) {
+        double area = out->areas[f];
+        if (out->tags[f] < 0) { if (area > amin) out->flags |= ORC_BOUNDARY; }
+        else if (area > amin) { ta[2 * nt] = (double)out->tags[f]; ta[2 * nt + 1] = area; nt++; }
     }
     qsort(ta, nt, 2 * sizeof(double), tagarea_cmp);
     out->nbr = (int32_t*)malloc(sizeof(int32_t) * (nt + 1));

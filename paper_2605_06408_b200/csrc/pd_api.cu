@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "../../include/pd.h"
@@ -102,10 +104,52 @@ T* to_result(pd_result* r, Arena& A, T* p) {
     return p;
 }
 
+// Pinned host buffers for PD_OUT_HOST results are recycled across builds (cudaMallocHost of a
+// ~1 GB CSR costs far more than the copy itself).  Buffers are keyed by capacity.
+struct PinnedCache {
+    std::mutex mu;
+    std::multimap<size_t, void*> free_;  // capacity -> buffer
+    std::map<void*, size_t> cap_;
+    size_t cached = 0;
+    static constexpr size_t kMaxCached = size_t(16) << 30;
+    void* get(size_t bytes) {
+        {
+            std::lock_guard<std::mutex> g(mu);
+            auto it = free_.lower_bound(bytes);
+            if (it != free_.end() && it->first <= 2 * bytes + (1 << 20)) {
+                void* p = it->second;
+                cached -= it->first;
+                free_.erase(it);
+                return p;
+            }
+        }
+        void* p = nullptr;
+        size_t cap = std::max<size_t>(bytes, 64);
+        ck(cudaMallocHost(&p, cap));
+        std::lock_guard<std::mutex> g(mu);
+        cap_[p] = cap;
+        return p;
+    }
+    void put(void* p) {
+        std::lock_guard<std::mutex> g(mu);
+        size_t cap = cap_[p];
+        if (cached + cap > kMaxCached) {
+            cap_.erase(p);
+            cudaFreeHost(p);
+            return;
+        }
+        free_.emplace(cap, p);
+        cached += cap;
+    }
+};
+PinnedCache& pinned() {
+    static PinnedCache c;
+    return c;
+}
+
 template <class T>
 T* host_copy(pd_result* r, const T* dptr, size_t count, cudaStream_t st) {
-    T* h = nullptr;
-    ck(cudaMallocHost(&h, std::max<size_t>(count * sizeof(T), 16)));
+    T* h = (T*)pinned().get(std::max<size_t>(count * sizeof(T), 16));
     r->host.push_back(h);
     if (count) ck(cudaMemcpyAsync(h, dptr, count * sizeof(T), cudaMemcpyDeviceToHost, st));
     return h;
@@ -118,7 +162,7 @@ void free_result(pd_result* r) {
     cudaSetDevice(r->device);
     for (void* p : r->dev) cudaFreeAsync(p, r->stream);
     if (!r->host.empty()) cudaStreamSynchronize(r->stream);
-    for (void* p : r->host) cudaFreeHost(p);
+    for (void* p : r->host) pinned().put(p);
     cudaSetDevice(cur);
     delete r;
 }
@@ -267,11 +311,12 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         int32_t* anbr = nullptr;
         float* aarea = nullptr;
         int sms = num_sms(opt.device);
-        const int spill_cap[3] = {2048, 8192, 65536};
+        const int spill_cap[3] = {2048, 8192, 32768};
         size_t spill_entries = 0;
         for (int t = 0; t < 3; ++t)
             spill_entries = std::max(spill_entries, (size_t)pd::cells_grid_warps(t, sms) * spill_cap[t]);
         pd::NodeChild* spill = A.alloc<pd::NodeChild>(spill_entries);
+        void* gstate = A.alloc<unsigned char>(pd::cells_global_state_bytes(sms));
         cudaEvent_t tev[4];
         for (auto& e : tev) ck(cudaEventCreate(&e));
         for (int attempt = 0; attempt < 3; ++attempt) {
@@ -308,6 +353,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.out.cost = cost;
             P.stats = dstats;
             P.spill = spill;
+            P.gstate = gstate;
             {
                 const char* ev = getenv("PD_EXACT_AFTER");  // tuning knob (default 200)
                 P.exact_after = ev ? atoi(ev) : 200;

@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "pd_internal.cuh"
 
 namespace pd {
@@ -38,8 +40,10 @@ constexpr unsigned FULL = 0xffffffffu;
 #define PD_EDGE_BITMAP 0
 #endif
 
-template <int V, int P, int Q, int W, int MINB>
+template <int V, int P, int Q, int W, int MINB, bool GLOB = false>
 struct TierCfg {
+    static constexpr bool GLOBAL = GLOB;     // warp state in global memory (top tier) instead of smem
+    using trip_t = typename std::conditional<(P <= 1024), uint32_t, uint64_t>::type;
     static constexpr int VMAX = V;   // vertices
     static constexpr int PMAX = P;   // planes (<= 1024: 10-bit triplet fields)
     static constexpr int QMAX = Q;   // on-chip priority-queue entries
@@ -57,14 +61,17 @@ struct TierCfg {
 #endif
 using Tier1 = TierCfg<96, 64, 64, 4, PD_T1_MINB>;
 using Tier2 = TierCfg<384, 192, 256, 4, 1>;
-using Tier3 = TierCfg<2048, 1024, 1024, 1, 1>;
+// Top tier: state in global memory (L1/L2-cached), 64-bit plane-index triplets; for the rare cells
+// with thousands of faces (heavy-tailed weights, SURVEY.md §7 hard part 3).
+using Tier3 = TierCfg<16384, 8192, 4096, 2, 1, true>;
+constexpr int kTier3BlocksPerSM = 1;
 
 template <class T>
 struct __align__(16) WarpState {
     double4 pl[T::PMAX];          // plane n.y <= d (n = p_j - p_i, local coordinates), exact
     float4 fv[T::VMAX];           // FP32 copy of the vertex positions (x, y, z, 0)
     double vx[T::VMAX], vy[T::VMAX], vz[T::VMAX];
-    uint32_t vt[T::VMAX];         // triplet a | b << 10 | c << 20, CCW seen from outside
+    typename T::trip_t vt[T::VMAX];  // plane-index triplet (a, b, c), CCW seen from outside
     int32_t pid[T::PMAX];         // >= 0 Morton index of the neighbour site; -1-k box wall k
     union {
         struct {                  // traversal: priority queue of pushed child records
@@ -75,6 +82,7 @@ struct __align__(16) WarpState {
             uint16_t tw[3][T::VMAX];  // twin vertex across edges a->b, b->c, c->a
             int32_t nb_id[T::PMAX];   // neighbour staging
             float nb_area[T::PMAX];
+            double farea[T::PMAX];    // face areas
         };
     };
     uint16_t rem[T::VMAX];        // removed-vertex slots of the current clip
@@ -91,12 +99,26 @@ __device__ __forceinline__ int ford(float f) {
 }
 __device__ __forceinline__ float iford(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
 
-__device__ __forceinline__ uint32_t tpack(int a, int b, int c) { return (uint32_t)a | ((uint32_t)b << 10) | ((uint32_t)c << 20); }
+// Plane-index triplets: 10-bit fields in a u32 (<= 1024 planes) or 21-bit fields in a u64.
+template <class TR>
+__device__ __forceinline__ TR tpack(int a, int b, int c);
+template <>
+__device__ __forceinline__ uint32_t tpack<uint32_t>(int a, int b, int c) {
+    return (uint32_t)a | ((uint32_t)b << 10) | ((uint32_t)c << 20);
+}
+template <>
+__device__ __forceinline__ uint64_t tpack<uint64_t>(int a, int b, int c) {
+    return (uint64_t)a | ((uint64_t)b << 21) | ((uint64_t)c << 42);
+}
 __device__ __forceinline__ int ta(uint32_t t) { return t & 1023; }
 __device__ __forceinline__ int tb(uint32_t t) { return (t >> 10) & 1023; }
 __device__ __forceinline__ int tc(uint32_t t) { return (t >> 20) & 1023; }
+__device__ __forceinline__ int ta(uint64_t t) { return (int)(t & 0x1fffff); }
+__device__ __forceinline__ int tb(uint64_t t) { return (int)((t >> 21) & 0x1fffff); }
+__device__ __forceinline__ int tc(uint64_t t) { return (int)((t >> 42) & 0x1fffff); }
 // does triplet t contain the directed dual edge x->y ?
-__device__ __forceinline__ bool has_edge(uint32_t t, int x, int y) {
+template <class TR>
+__device__ __forceinline__ bool has_edge(TR t, int x, int y) {
     int a = ta(t), b = tb(t), c = tc(t);
     return (a == x && b == y) || (b == x && c == y) || (c == x && a == y);
 }
@@ -272,7 +294,7 @@ __device__ __noinline__ void plane_gc(WarpState<T>& S, Cell& c, int lane) {
     for (int f = lane; f < c.np; f += 32) S.pmap[f] = 0;
     __syncwarp();
     for (int s = lane; s < c.nv; s += 32) {
-        uint32_t t = S.vt[s];
+        auto t = S.vt[s];
         S.pmap[ta(t)] = 1; S.pmap[tb(t)] = 1; S.pmap[tc(t)] = 1;
     }
     __syncwarp();
@@ -292,8 +314,8 @@ __device__ __noinline__ void plane_gc(WarpState<T>& S, Cell& c, int lane) {
     }
     __syncwarp();
     for (int s = lane; s < c.nv; s += 32) {
-        uint32_t t = S.vt[s];
-        S.vt[s] = tpack(S.pmap[ta(t)], S.pmap[tb(t)], S.pmap[tc(t)]);
+        auto t = S.vt[s];
+        S.vt[s] = tpack<typename T::trip_t>(S.pmap[ta(t)], S.pmap[tb(t)], S.pmap[tc(t)]);
     }
     c.np = base;
     __syncwarp();
@@ -345,7 +367,7 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double4 pl,
     //    its 3 unordered edges {x,y}; interior edges are toggled twice.  Large tiers: pairwise scan.
     if (T::EDGE_BITMAP) {
         for (int r = lane; r < R; r += 32) {
-            uint32_t t = S.vt[S.rem[r]];
+            auto t = S.vt[S.rem[r]];
             int a = ta(t), b = tb(t), cc = tc(t);
             int k0 = min(a, b) * T::PMAX + max(a, b), k1 = min(b, cc) * T::PMAX + max(b, cc),
                 k2 = min(cc, a) * T::PMAX + max(cc, a);
@@ -361,7 +383,7 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double4 pl,
         int nb = 0;
         uint32_t e0 = 0, e1 = 0, e2 = 0;
         if (r < R) {
-            uint32_t t = S.vt[S.rem[r]];
+            auto t = S.vt[S.rem[r]];
             int a = ta(t), b = tb(t), cc = tc(t);
             bool f0 = false, f1 = false, f2 = false;
             if (T::EDGE_BITMAP) {
@@ -373,7 +395,7 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double4 pl,
             } else {
 #pragma unroll 1
                 for (int k = 0; k < R; ++k) {
-                    uint32_t u = S.vt[S.rem[k]];
+                    auto u = S.vt[S.rem[k]];
                     f0 |= has_edge(u, b, a);
                     f1 |= has_edge(u, cc, b);
                     f2 |= has_edge(u, a, cc);
@@ -404,7 +426,7 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double4 pl,
     if (T::EDGE_BITMAP) {  // restore the all-zero bitmap
         __syncwarp();
         for (int r = lane; r < R; r += 32) {
-            uint32_t t = S.vt[S.rem[r]];
+            auto t = S.vt[S.rem[r]];
             int a = ta(t), b = tb(t), cc = tc(t);
             S.ebits[(min(a, b) * T::PMAX + max(a, b)) >> 5] = 0u;
             S.ebits[(min(b, cc) * T::PMAX + max(b, cc)) >> 5] = 0u;
@@ -430,7 +452,7 @@ __device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double4 pl,
             solve3(pl, S.pl[x], S.pl[y], vx, vy, vz);
             int slot = e < R ? S.rem[e] : c.nv + (e - R);
             put_vertex(S.fv, S.vx, S.vy, S.vz, slot, vx, vy, vz);
-            S.vt[slot] = tpack(hs, x, y);
+            S.vt[slot] = tpack<typename T::trip_t>(hs, x, y);
         }
     }
     // 4. if fewer vertices were created than removed, move kept vertices from the tail into holes
@@ -730,7 +752,7 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
         put_vertex(S.fv, S.vx, S.vy, S.vz, lane, sx ? hi[0] : lo[0], sy ? hi[1] : lo[1], sz ? hi[2] : lo[2]);
         int X = sx, Y = 2 + sy, Z = 4 + sz;
         int sgn = (sx ? 1 : -1) * (sy ? 1 : -1) * (sz ? 1 : -1);  // det of the outward normals
-        S.vt[lane] = sgn > 0 ? tpack(X, Y, Z) : tpack(X, Z, Y);
+        S.vt[lane] = sgn > 0 ? tpack<typename T::trip_t>(X, Y, Z) : tpack<typename T::trip_t>(X, Z, Y);
     }
     c.nv = 8;
     c.np = 6;
@@ -757,12 +779,12 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
     }
     // twins: vertex across each directed edge
     for (int u = lane; u < c.nv; u += 32) {
-        uint32_t t = S.vt[u];
+        auto t = S.vt[u];
         int a = ta(t), b = tb(t), cc = tc(t);
         uint16_t t0 = 0xffff, t1 = 0xffff, t2 = 0xffff;
 #pragma unroll 1
         for (int k = 0; k < c.nv; ++k) {
-            uint32_t w = S.vt[k];
+            auto w = S.vt[k];
             if (has_edge(w, b, a)) t0 = (uint16_t)k;
             if (has_edge(w, cc, b)) t1 = (uint16_t)k;
             if (has_edge(w, a, cc)) t2 = (uint16_t)k;
@@ -771,15 +793,13 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
     }
     __syncwarp();
     double vol = 0, surf = 0;
-    bool boundary = false;
-    int K = 0;
     for (int f0 = 0; f0 < c.np; f0 += 32) {
         int f = f0 + lane;
         double Ax = 0, Ay = 0, Az = 0;
         if (f < c.np) {
 #pragma unroll 1
             for (int u = 0; u < c.nv; ++u) {
-                uint32_t t = S.vt[u];
+                auto t = S.vt[u];
                 int which = ta(t) == f ? 2 : (tb(t) == f ? 0 : (tc(t) == f ? 1 : -1));
                 if (which >= 0) {
                     int w = S.tw[which][u];
@@ -791,18 +811,33 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
                     Az += ux * wy - uy * wx;
                 }
             }
-        }
-        Ax *= 0.5; Ay *= 0.5; Az *= 0.5;
-        double area = sqrt(Ax * Ax + Ay * Ay + Az * Az);
-        bool nb = false;
-        if (f < c.np && area > 0) {
+            Ax *= 0.5; Ay *= 0.5; Az *= 0.5;
+            double area = sqrt(Ax * Ax + Ay * Ay + Az * Az);
+            S.farea[f] = area;
             double4 pl = S.pl[f];
             double nn = pl.x * pl.x + pl.y * pl.y + pl.z * pl.z;
             vol += (Ax * pl.x + Ay * pl.y + Az * pl.z) * pl.w / nn;
             surf += area;
-            int id = S.pid[f];
-            if (id < 0) boundary = true;
-            else nb = true;
+        }
+    }
+    vol = warp_sum_d(vol) / 3.0;
+    surf = warp_sum_d(surf);
+    __syncwarp();
+    // A face counts when its area exceeds 1e-13 S: below that it is a rounding artefact of a
+    // zero-area (edge / vertex) contact of a degenerate configuration (reading R2).
+    const double amin = 1e-13 * surf;
+    bool boundary = false;
+    int K = 0;
+    for (int f0 = 0; f0 < c.np; f0 += 32) {
+        int f = f0 + lane;
+        bool nb = false;
+        double area = 0;
+        if (f < c.np) {
+            area = S.farea[f];
+            if (area > amin) {
+                if (S.pid[f] < 0) boundary = true;
+                else nb = true;
+            }
         }
         unsigned mb = __ballot_sync(FULL, nb);
         if (nb) {
@@ -812,8 +847,6 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
         }
         K += __popc(mb);
     }
-    vol = warp_sum_d(vol) / 3.0;
-    surf = warp_sum_d(surf);
     boundary = __any_sync(FULL, boundary);
     __syncwarp();
     // arena row (ascending original ids)
@@ -846,7 +879,8 @@ template <class T>
 __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(CellParams P, int tier) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    WarpState<T>& S = reinterpret_cast<WarpState<T>*>(smem_raw)[wid];
+    WarpState<T>& S = T::GLOBAL ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x * T::WARPS + wid]
+                                : reinterpret_cast<WarpState<T>*>(smem_raw)[wid];
     const int64_t total = P.list ? (int64_t)(*P.list_count) : P.count;
     Counters cnt = {0, 0, 0, 0, 0, 0};
     const int gw = blockIdx.x * T::WARPS + wid;
@@ -905,6 +939,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
 
 template <class T>
 int tier_grid(int num_sms) {
+    if (T::GLOBAL) return num_sms * kTier3BlocksPerSM;
     size_t smem = sizeof(WarpState<T>) * T::WARPS;
     cudaFuncSetAttribute(cells_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
@@ -915,7 +950,7 @@ int tier_grid(int num_sms) {
 
 template <class T>
 cudaError_t launch_tier(const CellParams& p, int tier, cudaStream_t st, int num_sms) {
-    size_t smem = sizeof(WarpState<T>) * T::WARPS;
+    size_t smem = T::GLOBAL ? 0 : sizeof(WarpState<T>) * T::WARPS;
     int grid = tier_grid<T>(num_sms);
     cells_kernel<T><<<grid, T::WARPS * 32, smem, st>>>(p, tier);
     return cudaGetLastError();
@@ -928,6 +963,10 @@ cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num
     if (tier == 0) return launch_tier<Tier1>(p, 0, st, num_sms);
     if (tier == 1) return launch_tier<Tier2>(p, 1, st, num_sms);
     return launch_tier<Tier3>(p, 2, st, num_sms);
+}
+
+size_t cells_global_state_bytes(int num_sms) {
+    return (size_t)tier_grid<Tier3>(num_sms) * Tier3::WARPS * sizeof(WarpState<Tier3>);
 }
 
 int cells_grid_warps(int tier, int num_sms) {

@@ -75,9 +75,11 @@ struct CellParams {
     NodeChild* spill;   // per-warp queue spill stacks (global memory)
     int spill_cap;      // entries per warp
     int exact_after;    // exact node tests once a cell has visited this many nodes
+    void* gstate;       // top tier: per-warp cell state in global memory
 };
 
 cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches);
 int cells_grid_warps(int tier, int num_sms);
+size_t cells_global_state_bytes(int num_sms);
 
 }  // namespace pd
