@@ -95,6 +95,7 @@ typedef struct {
     int64_t nnz;               /* total neighbour entries */
     double ms_bvh, ms_cells, ms_csr, ms_total; /* phase times (CUDA events) */
     double ms_tier[3];         /* cell-kernel time per capacity tier (CUDA events) */
+    int64_t warp_cycles[6];    /* PD_PROFILE builds only: warp clock64 in init/descend/leaf/clip/pop/finalize */
 } pd_stats;
 
 typedef struct pd_result pd_result;

@@ -52,12 +52,14 @@ class Stats(ctypes.Structure):
                 ("tier_cells", ctypes.c_int64 * 3), ("overflow_cells", ctypes.c_int64), ("queue_spills", ctypes.c_int64),
                 ("nnz", ctypes.c_int64),
                 ("ms_bvh", ctypes.c_double), ("ms_cells", ctypes.c_double), ("ms_csr", ctypes.c_double),
-                ("ms_total", ctypes.c_double), ("ms_tier", ctypes.c_double * 3)]
+                ("ms_total", ctypes.c_double), ("ms_tier", ctypes.c_double * 3),
+                ("warp_cycles", ctypes.c_int64 * 6)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
         d["tier_cells"] = list(self.tier_cells)
         d["ms_tier"] = list(self.ms_tier)
+        d["warp_cycles"] = list(self.warp_cycles)
         return d
 
 

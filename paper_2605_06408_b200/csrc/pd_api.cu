@@ -439,6 +439,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         for (int k = 0; k < 3; ++k) s.tier_cells[k] = (int64_t)hs.tier[k];
         s.overflow_cells = (int64_t)hs.overflow;
         s.queue_spills = (int64_t)hs.spills;
+        for (int k = 0; k < 6; ++k) s.warp_cycles[k] = (int64_t)hs.cyc[k];
         s.nnz = nnz;
         s.ms_bvh = t01;
         s.ms_cells = t12;

@@ -36,6 +36,15 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef PD_INL_CLIP
+#define PD_INL_CLIP __noinline__
+#endif
+#ifndef PD_INL_LEAF
+#define PD_INL_LEAF __noinline__
+#endif
+#ifndef PD_EXACT_LEAVES
+#define PD_EXACT_LEAVES 0
+#endif
 #ifndef PD_EDGE_BITMAP
 #define PD_EDGE_BITMAP 0
 #endif
@@ -59,15 +68,36 @@ struct TierCfg {
 #ifndef PD_T1_MINB
 #define PD_T1_MINB 5
 #endif
-using Tier1 = TierCfg<96, 64, 64, 4, PD_T1_MINB>;
+#ifndef PD_T1_Q
+#define PD_T1_Q 64
+#endif
+#ifndef PD_T1_V
+#define PD_T1_V 96
+#endif
+using Tier1 = TierCfg<PD_T1_V, 64, PD_T1_Q, 4, PD_T1_MINB>;
 using Tier2 = TierCfg<384, 192, 256, 4, 1>;
 // Top tier: state in global memory (L1/L2-cached), 64-bit plane-index triplets; for the rare cells
 // with thousands of faces (heavy-tailed weights, SURVEY.md §7 hard part 3).
 using Tier3 = TierCfg<16384, 8192, 4096, 2, 1, true>;
 constexpr int kTier3BlocksPerSM = 1;
 
+// Per-warp cell state (warp-uniform).  Lives in the warp's shared-memory block (read by broadcast):
+// passing a register-resident struct by reference to non-inlined functions would put it on the
+// thread stack (local memory), which thrashes L1 once shared memory takes the carveout.
+struct Cell {
+    double px, py, pz, pw;  // site (world), weight
+    float fpx, fpy, fpz, fpw;
+    float flo[3], fhi[3];   // cell AABB, site-local, rounded outward
+    float vmax;             // max_k max(|lo_k|, |hi_k|)
+    float rmax;             // max corner distance of the AABB (isotropic radius bound)
+    int nv, np, nq;
+    int self;               // Morton index
+    int self_orig;
+};
+
 template <class T>
 struct __align__(16) WarpState {
+    Cell c;                       // warp-uniform cell state
     double4 pl[T::PMAX];          // plane n.y <= d (n = p_j - p_i, local coordinates), exact
     float4 fv[T::VMAX];           // FP32 copy of the vertex positions (x, y, z, 0)
     double vx[T::VMAX], vy[T::VMAX], vz[T::VMAX];
@@ -150,6 +180,16 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     return v;
 }
 
+// Compile-time culling/traversal mode.  Tier 1 is instantiated per common mode so that the default
+// kernel carries none of the ablation branches (instruction-fetch stalls dominate otherwise);
+// kDynMode reads the mode bits from the runtime flags (mode combinations, tiers 2-3).
+constexpr unsigned kModeBits = PD_ISOTROPIC | PD_DFS | PD_PAPER_BOUND | PD_EXACT_NODES | PD_NO_EXACT;
+constexpr unsigned kDynMode = 0xffffffffu;
+template <unsigned MODE>
+__device__ __forceinline__ unsigned mode_flags(unsigned runtime_flags) {
+    return MODE == kDynMode ? runtime_flags : (MODE | (runtime_flags & ~kModeBits));
+}
+
 // Exact node tests switch on once a cell has visited `after` nodes (heavy cells), or always with
 // PD_EXACT_NODES; PD_NO_EXACT disables them.
 __device__ __forceinline__ bool exact_on(unsigned flags, unsigned long long visited, int after) {
@@ -162,19 +202,19 @@ enum { CLIP_NONE = 0, CLIP_DONE = 1, CLIP_EMPTY = 2, CLIP_OVF = 3 };
 
 struct Counters {
     unsigned long long nodes, leaves, sites, tests, clips, spills;
+    unsigned long long cyc[6];  // PD_PROFILE builds: warp cycles in init, descend, leaf, clip, pop, finalize
 };
+#ifndef PD_PROFILE
+#define PD_PROFILE 0
+#endif
+#if PD_PROFILE
+#define PT_BEGIN(v) long long v = clock64()
+#define PT_END(v, k) cnt.cyc[k] += (unsigned long long)(clock64() - v)
+#else
+#define PT_BEGIN(v) (void)0
+#define PT_END(v, k) (void)0
+#endif
 
-// Per-warp register state (identical in all lanes).
-struct Cell {
-    double px, py, pz, pw;  // site (world), weight
-    float fpx, fpy, fpz, fpw;
-    float flo[3], fhi[3];   // cell AABB, site-local, rounded outward
-    float vmax;             // max_k max(|lo_k|, |hi_k|)
-    float rmax;             // max corner distance of the AABB (isotropic radius bound)
-    int nv, np, nq;
-    int self;               // Morton index
-    int self_orig;
-};
 
 // An FP32 plane with its certification margin: |s32 - s| <= err < m for s = n.v - d evaluated in
 // FP32 from the FP32 copies (all inputs carry <= 2^-24 relative rounding; the FMA chain adds a few
@@ -343,7 +383,7 @@ __device__ __forceinline__ bool outside(const WarpState<T>& S, int s, const FPla
 
 // Clip the cell by {y : n.y <= d} (re-designed warp-parallel).
 template <class T>
-__device__ __noinline__ int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, double tol, FPlane f, int pidn) {
+__device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, double tol, FPlane f, int pidn) {
     if (c.np >= (T::PMAX * 85) / 100) {
         plane_gc(S, c, lane);
         if (c.np >= T::PMAX) return CLIP_OVF;
@@ -502,8 +542,20 @@ __device__ __forceinline__ bool site_culled(const Cell& c, float Dx, float Dy, f
     return q - 2.f * rd > 1e-5f * (D2 + fabsf(dq) + 2.f * rd);
 }
 
+// FP64 certification of a candidate whose FP32 cut test was ambiguous (rare; kept out of line).
 template <class T>
-__device__ __noinline__ int process_leaf(WarpState<T>& S, Cell& c, int lane, int link, const CellParams& P, Counters& cnt) {
+__device__ __noinline__ bool cuts_fp64(const WarpState<T>& S, const Cell& c, float4 sj, float D2) {
+    double ex = (double)sj.x - c.px, ey = (double)sj.y - c.py, ez = (double)sj.z - c.pz;
+    double ed = 0.5 * (ex * ex + ey * ey + ez * ez + (c.pw - (double)sj.w));
+    double tol = 1e-12 * (double)sqrtf(D2) * (double)c.rmax;
+    for (int k = 0; k < c.nv; ++k)
+        if (fma(ex, S.vx[k], fma(ey, S.vy[k], ez * S.vz[k])) - ed > tol) return true;
+    return false;
+}
+
+template <class T, unsigned MODE>
+__device__ PD_INL_LEAF int process_leaf(WarpState<T>& S, Cell& c, int lane, int link, const CellParams& P, Counters& cnt) {
+    const unsigned flags = mode_flags<MODE>(P.flags);
     const int first = leaf_first(link), count = leaf_count(link);
     const int j = first + lane;
     bool valid = lane < count && j != c.self;
@@ -523,7 +575,7 @@ __device__ __noinline__ int process_leaf(WarpState<T>& S, Cell& c, int lane, int
     }
     if (__any_sync(FULL, dup_kill)) return ST_DUP;
     cnt.sites += count;
-    bool cand = valid && !site_culled(c, Dx, Dy, Dz, D2, dq, P.flags);
+    bool cand = valid && !site_culled(c, Dx, Dy, Dz, D2, dq, flags);
     unsigned mask = __ballot_sync(FULL, cand);
     if (!mask) return ST_OK;
     // Batch cut test, lane = candidate: does the plane cut the CURRENT cell?  A plane that does not
@@ -541,13 +593,7 @@ __device__ __noinline__ int process_leaf(WarpState<T>& S, Cell& c, int lane, int
                 cuts |= s > m;
                 amb |= fabsf(s) <= m;
             }
-            if (!cuts && amb) {  // certify in FP64 (rare)
-                double ex = (double)sj.x - c.px, ey = (double)sj.y - c.py, ez = (double)sj.z - c.pz;
-                double ed = 0.5 * (ex * ex + ey * ey + ez * ez + (c.pw - (double)sj.w));
-                double tol = 1e-12 * (double)sqrtf(D2) * (double)c.rmax;
-                for (int k = 0; k < c.nv && !cuts; ++k)
-                    cuts = fma(ex, S.vx[k], fma(ey, S.vy[k], ez * S.vz[k])) - ed > tol;
-            }
+            if (!cuts && amb) cuts = cuts_fp64(S, c, sj, D2);  // certify in FP64 (rare)
         }
         cnt.tests += __popc(mask);
         cand = cand && cuts;
@@ -571,12 +617,14 @@ __device__ __noinline__ int process_leaf(WarpState<T>& S, Cell& c, int lane, int
         float f2 = f.nx * f.nx + f.ny * f.ny + f.nz * f.nz, fdq = c.fpw - sw;
         f.d = 0.5f * (f2 + fdq);
         f.m = 1e-6f * ((fabsf(f.nx) + fabsf(f.ny) + fabsf(f.nz)) * c.vmax + f2 + fabsf(fdq));
+        PT_BEGIN(t_clip);
         int st = clip(S, c, lane, pl, tol, f, first + src);
+        PT_END(t_clip, 3);
         if (st == CLIP_EMPTY) return ST_EMPTY;
         if (st == CLIP_OVF) return ST_OVERFLOW;
         if (st == CLIP_DONE) {
             cnt.clips++;
-            if (cand && site_culled(c, Dx, Dy, Dz, D2, dq, P.flags)) cand = false;
+            if (cand && site_culled(c, Dx, Dy, Dz, D2, dq, flags)) cand = false;
         }
         mask = __ballot_sync(FULL, cand);
     }
@@ -586,10 +634,11 @@ __device__ __noinline__ int process_leaf(WarpState<T>& S, Cell& c, int lane, int
 // Best-first traversal (Alg. 1).  Queue entries are the pushed child records;
 // when the on-chip queue is full, entries spill to a per-warp stack in global memory (order is
 // relaxed, correctness is not affected) and are refilled when the on-chip queue drains.
-template <class T>
+template <class T, unsigned MODE>
 __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P, Counters& cnt, NodeChild* spill,
                         int spill_cap) {
-    const bool dfs = (P.flags & PD_DFS) != 0;
+    const unsigned flags = mode_flags<MODE>(P.flags);
+    const bool dfs = (flags & PD_DFS) != 0;
     int node = __float_as_int(__ldg(&P.root->hi_l.w));
     bool have = true;
     int ns = 0;  // spilled entries
@@ -597,6 +646,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
     c.nq = 0;
     for (;;) {
         if (have) {
+            PT_BEGIN(t_desc);
             while (node >= 0) {  // descend (Alg. 1 lines 4-18), 8 children per visit
                 cnt.nodes++;
                 float key = INFINITY;
@@ -606,11 +656,16 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 if (lane < WIDE) {
                     lo_w = __ldg(&rec[lane].lo_w);
                     hi_l = __ldg(&rec[lane].hi_l);
-                    if (__float_as_int(hi_l.w) != EMPTY_LINK) key = node_test(c, lo_w, hi_l, P.flags, culled);
+                    if (__float_as_int(hi_l.w) != EMPTY_LINK) key = node_test(c, lo_w, hi_l, flags, culled);
                 }
                 unsigned surv = __ballot_sync(FULL, !culled);
-                if (surv && exact_on(P.flags, cnt.nodes - nodes0, P.exact_after)) {
-                    unsigned s2 = surv;
+                const bool ex_all = exact_on(flags, cnt.nodes - nodes0, P.exact_after);
+                // exact test on every surviving LEAF child (a leaf costs far more than the test), and on
+                // internal children too once the cell is heavy
+                const unsigned leafm = __ballot_sync(FULL, lane < WIDE && __float_as_int(hi_l.w) < 0);
+                const unsigned exm = ex_all ? surv : (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) ? (surv & leafm) : 0u);
+                if (exm) {
+                    unsigned s2 = exm;
                     while (s2) {
                         int k = __ffs(s2) - 1;
                         s2 &= s2 - 1;
@@ -647,13 +702,17 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 node = lnear;
             }
             if (have) {
+                PT_END(t_desc, 1);
                 cnt.leaves++;
                 __syncwarp();
-                int st = process_leaf(S, c, lane, node, P, cnt);
+                PT_BEGIN(t_leaf);
+                int st = process_leaf<T, MODE>(S, c, lane, node, P, cnt);
+                PT_END(t_leaf, 2);
                 if (st != ST_OK) return st;
             }
         }
         // pop (Alg. 1 lines 21-31): re-validate every queued entry against the shrunk cell
+        PT_BEGIN(t_pop);
         __syncwarp();
         if (c.nq == 0 && ns > 0) {  // refill from the spill stack
             __threadfence_block();
@@ -673,7 +732,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             while (c.nq > 0 && !ok) {
                 int t = c.nq - 1;
                 bool culled;
-                node_test(c, S.qlo[t], S.qhi[t], P.flags, culled);
+                node_test(c, S.qlo[t], S.qhi[t], flags, culled);
                 node = __float_as_int(S.qhi[t].w);
                 c.nq--;
                 ok = !culled;
@@ -693,7 +752,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             bool al = false;
             if (s < c.nq) {
                 bool culled;
-                float k = node_test(c, S.qlo[s], S.qhi[s], P.flags, culled);
+                float k = node_test(c, S.qlo[s], S.qhi[s], flags, culled);
                 al = !culled;
                 if (al && ford(k) < bestk) { bestk = ford(k); bests = s; }
             }
@@ -711,7 +770,8 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         unsigned lead = __ballot_sync(FULL, bestk == gk);
         int bslot = __shfl_sync(FULL, bests, __ffs(lead) - 1);
         node = __float_as_int(S.qhi[bslot].w);
-        bool popped_dead = exact_on(P.flags, cnt.nodes - nodes0, P.exact_after) &&
+        bool popped_dead = (exact_on(flags, cnt.nodes - nodes0, P.exact_after) ||
+                            (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) && node < 0)) &&
                            node_exact_culled(S, c, lane, S.qlo[bslot], S.qhi[bslot]);
         // compact: keep alive entries except the popped one
         int base = 0;
@@ -732,6 +792,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         }
         c.nq = base;
         have = !popped_dead;
+        PT_END(t_pop, 4);
     }
 }
 
@@ -875,14 +936,14 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
     }
 }
 
-template <class T>
+template <class T, unsigned MODE>
 __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(CellParams P, int tier) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     WarpState<T>& S = T::GLOBAL ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x * T::WARPS + wid]
                                 : reinterpret_cast<WarpState<T>*>(smem_raw)[wid];
     const int64_t total = P.list ? (int64_t)(*P.list_count) : P.count;
-    Counters cnt = {0, 0, 0, 0, 0, 0};
+    Counters cnt = {0, 0, 0, 0, 0, 0, {0, 0, 0, 0, 0, 0}};
     const int gw = blockIdx.x * T::WARPS + wid;
     NodeChild* spill = P.spill + (size_t)gw * P.spill_cap;
     for (int k = lane; k < T::EBW; k += 32) S.ebits[k] = 0u;
@@ -897,15 +958,17 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
         for (int b = 0; b < BATCH && b0 + b < total; ++b) {
             int64_t idx = b0 + b;
             int s = P.list ? P.list[idx] : (int)(P.begin + idx);
-            Cell c;
+            Cell& c = S.c;
             const Counters before = cnt;
             float4 site = __ldg(&P.sites[s]);
             c.fpx = site.x; c.fpy = site.y; c.fpz = site.z; c.fpw = site.w;
             c.px = site.x; c.py = site.y; c.pz = site.z; c.pw = site.w;
             c.self = s;
             c.self_orig = __ldg(&P.perm[s]);
+            PT_BEGIN(t_init);
             init_cell(S, c, lane, P);
-            int st = traverse(S, c, lane, P, cnt, spill, P.spill_cap);
+            PT_END(t_init, 0);
+            int st = traverse<T, MODE>(S, c, lane, P, cnt, spill, P.spill_cap);
             __syncwarp();
             if (st == ST_OVERFLOW && !P.last_tier) {
                 if (lane == 0) {
@@ -915,7 +978,9 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
                 continue;
             }
             if (st == ST_OVERFLOW) novf++;
+            PT_BEGIN(t_fin);
             finalize(S, c, lane, P, st);
+            PT_END(t_fin, 5);
             ncells++;
             if ((P.flags & PD_COST) && lane == 0) {
                 unsigned long long w = (cnt.nodes - before.nodes) + (cnt.sites - before.sites) + 8 * (cnt.clips - before.clips);
@@ -934,25 +999,26 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
         red_add_g(&P.stats->tier[tier], ncells);
         red_add_g(&P.stats->overflow, novf);
         red_add_g(&P.stats->spills, cnt.spills);
+        for (int k = 0; k < 6; ++k) red_add_g(&P.stats->cyc[k], cnt.cyc[k]);
     }
 }
 
-template <class T>
+template <class T, unsigned MODE>
 int tier_grid(int num_sms) {
     if (T::GLOBAL) return num_sms * kTier3BlocksPerSM;
     size_t smem = sizeof(WarpState<T>) * T::WARPS;
-    cudaFuncSetAttribute(cells_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(cells_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cells_kernel<T>, T::WARPS * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cells_kernel<T, MODE>, T::WARPS * 32, smem);
     if (per_sm < 1) per_sm = 1;
     return num_sms * per_sm;
 }
 
-template <class T>
+template <class T, unsigned MODE>
 cudaError_t launch_tier(const CellParams& p, int tier, cudaStream_t st, int num_sms) {
     size_t smem = T::GLOBAL ? 0 : sizeof(WarpState<T>) * T::WARPS;
-    int grid = tier_grid<T>(num_sms);
-    cells_kernel<T><<<grid, T::WARPS * 32, smem, st>>>(p, tier);
+    int grid = tier_grid<T, MODE>(num_sms);
+    cells_kernel<T, MODE><<<grid, T::WARPS * 32, smem, st>>>(p, tier);
     return cudaGetLastError();
 }
 
@@ -960,19 +1026,35 @@ cudaError_t launch_tier(const CellParams& p, int tier, cudaStream_t st, int num_
 
 cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches) {
     if (launches) ++*launches;
-    if (tier == 0) return launch_tier<Tier1>(p, 0, st, num_sms);
-    if (tier == 1) return launch_tier<Tier2>(p, 1, st, num_sms);
-    return launch_tier<Tier3>(p, 2, st, num_sms);
+    if (tier == 0) {
+        switch (p.flags & kModeBits) {  // tier 1: specialized kernels for the common modes
+            case 0: return launch_tier<Tier1, 0u>(p, 0, st, num_sms);
+            case PD_PAPER_BOUND: return launch_tier<Tier1, PD_PAPER_BOUND>(p, 0, st, num_sms);
+            case PD_ISOTROPIC: return launch_tier<Tier1, PD_ISOTROPIC>(p, 0, st, num_sms);
+            case PD_DFS: return launch_tier<Tier1, PD_DFS>(p, 0, st, num_sms);
+            default: return launch_tier<Tier1, kDynMode>(p, 0, st, num_sms);
+        }
+    }
+    if (tier == 1) return launch_tier<Tier2, kDynMode>(p, 1, st, num_sms);
+    return launch_tier<Tier3, kDynMode>(p, 2, st, num_sms);
 }
 
 size_t cells_global_state_bytes(int num_sms) {
-    return (size_t)tier_grid<Tier3>(num_sms) * Tier3::WARPS * sizeof(WarpState<Tier3>);
+    return (size_t)tier_grid<Tier3, kDynMode>(num_sms) * Tier3::WARPS * sizeof(WarpState<Tier3>);
 }
 
 int cells_grid_warps(int tier, int num_sms) {
-    if (tier == 0) return tier_grid<Tier1>(num_sms) * Tier1::WARPS;
-    if (tier == 1) return tier_grid<Tier2>(num_sms) * Tier2::WARPS;
-    return tier_grid<Tier3>(num_sms) * Tier3::WARPS;
+    // all tier-1 instantiations share one register/smem footprint bound; take the largest grid
+    if (tier == 0) {
+        int g = tier_grid<Tier1, 0u>(num_sms);
+        g = max(g, tier_grid<Tier1, PD_PAPER_BOUND>(num_sms));
+        g = max(g, tier_grid<Tier1, PD_ISOTROPIC>(num_sms));
+        g = max(g, tier_grid<Tier1, PD_DFS>(num_sms));
+        g = max(g, tier_grid<Tier1, kDynMode>(num_sms));
+        return g * Tier1::WARPS;
+    }
+    if (tier == 1) return tier_grid<Tier2, kDynMode>(num_sms) * Tier2::WARPS;
+    return tier_grid<Tier3, kDynMode>(num_sms) * Tier3::WARPS;
 }
 
 }  // namespace pd
