@@ -36,11 +36,14 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef PD_INL_AABB
+#define PD_INL_AABB __forceinline__
+#endif
 #ifndef PD_INL_CLIP
-#define PD_INL_CLIP __noinline__
+#define PD_INL_CLIP __forceinline__
 #endif
 #ifndef PD_INL_LEAF
-#define PD_INL_LEAF __noinline__
+#define PD_INL_LEAF __forceinline__
 #endif
 #ifndef PD_EXACT_LEAVES
 #define PD_EXACT_LEAVES 0
@@ -296,7 +299,7 @@ __device__ __noinline__ bool node_exact_culled(const WarpState<T>& S, const Cell
 }
 
 template <class T>
-__device__ __noinline__ void update_aabb(const WarpState<T>& S, Cell& c, int lane) {
+__device__ PD_INL_AABB void update_aabb(const WarpState<T>& S, Cell& c, int lane) {
     float lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY;
     for (int s = lane; s < c.nv; s += 32) {
         float4 v = S.fv[s];
