@@ -36,6 +36,12 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef PD_MATCH
+#define PD_MATCH 1
+#endif
+#ifndef PD_FUSED_AABB
+#define PD_FUSED_AABB 0
+#endif
 #ifndef PD_INL_AABB
 #define PD_INL_AABB __forceinline__
 #endif
@@ -298,15 +304,23 @@ __device__ __noinline__ bool node_exact_culled(const WarpState<T>& S, const Cell
     return best < 0.5f * (c.fpw - lo_w.w) - 1e-5f * mag;
 }
 
-template <class T>
-__device__ PD_INL_AABB void update_aabb(const WarpState<T>& S, Cell& c, int lane) {
-    float lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY;
-    for (int s = lane; s < c.nv; s += 32) {
-        float4 v = S.fv[s];
+// Per-lane partial AABB of vertex positions (FP32 copies).
+struct Box6 {
+    float lo0, lo1, lo2, hi0, hi1, hi2;
+    __device__ __forceinline__ void reset() {
+        lo0 = lo1 = lo2 = INFINITY;
+        hi0 = hi1 = hi2 = -INFINITY;
+    }
+    __device__ __forceinline__ void add(float4 v) {
         lo0 = fminf(lo0, v.x); hi0 = fmaxf(hi0, v.x);
         lo1 = fminf(lo1, v.y); hi1 = fmaxf(hi1, v.y);
         lo2 = fminf(lo2, v.z); hi2 = fmaxf(hi2, v.z);
     }
+};
+
+// Warp-reduce the partial boxes into the cell AABB (widened by 2 ulp) and its radius bounds.
+__device__ __forceinline__ void finish_aabb(Cell& c, const Box6& b) {
+    float lo0 = b.lo0, lo1 = b.lo1, lo2 = b.lo2, hi0 = b.hi0, hi1 = b.hi1, hi2 = b.hi2;
     c.flo[0] = iford(__reduce_min_sync(FULL, ford(lo0)));
     c.flo[1] = iford(__reduce_min_sync(FULL, ford(lo1)));
     c.flo[2] = iford(__reduce_min_sync(FULL, ford(lo2)));
@@ -326,6 +340,14 @@ __device__ PD_INL_AABB void update_aabb(const WarpState<T>& S, Cell& c, int lane
     c.vmax = vm;
 }
 
+template <class T>
+__device__ PD_INL_AABB void update_aabb(const WarpState<T>& S, Cell& c, int lane) {
+    Box6 b;
+    b.reset();
+    for (int s = lane; s < c.nv; s += 32) b.add(S.fv[s]);
+    finish_aabb(c, b);
+}
+
 __device__ __forceinline__ void put_vertex(float4* fv, double* vx, double* vy, double* vz, int s, double x, double y, double z) {
     vx[s] = x; vy[s] = y; vz[s] = z;
     fv[s] = make_float4((float)x, (float)y, (float)z, 0.f);
@@ -334,17 +356,18 @@ __device__ __forceinline__ void put_vertex(float4* fv, double* vx, double* vy, d
 // Plane garbage collection: drop planes no vertex references.
 template <class T>
 __device__ __noinline__ void plane_gc(WarpState<T>& S, Cell& c, int lane) {
-    for (int f = lane; f < c.np; f += 32) S.pmap[f] = 0;
+    const int np0 = c.np, nv0 = c.nv;
+    for (int f = lane; f < np0; f += 32) S.pmap[f] = 0;
     __syncwarp();
-    for (int s = lane; s < c.nv; s += 32) {
+    for (int s = lane; s < nv0; s += 32) {
         auto t = S.vt[s];
         S.pmap[ta(t)] = 1; S.pmap[tb(t)] = 1; S.pmap[tc(t)] = 1;
     }
     __syncwarp();
     int base = 0;
-    for (int f0 = 0; f0 < c.np; f0 += 32) {
+    for (int f0 = 0; f0 < np0; f0 += 32) {
         int f = f0 + lane;
-        bool live = f < c.np && S.pmap[f];
+        bool live = f < np0 && S.pmap[f];
         unsigned m = __ballot_sync(FULL, live);
         int dst = base + __popc(m & lanemask_lt());
         double4 pl;
@@ -356,7 +379,7 @@ __device__ __noinline__ void plane_gc(WarpState<T>& S, Cell& c, int lane) {
         base += __popc(m);
     }
     __syncwarp();
-    for (int s = lane; s < c.nv; s += 32) {
+    for (int s = lane; s < nv0; s += 32) {
         auto t = S.vt[s];
         S.vt[s] = tpack<typename T::trip_t>(S.pmap[ta(t)], S.pmap[tb(t)], S.pmap[tc(t)]);
     }
@@ -375,15 +398,6 @@ __device__ __forceinline__ void solve3(double4 a, double4 b, double4 c, double& 
     z = (a.w * bcz + b.w * caz + c.w * abz) * inv;
 }
 
-// Is vertex s strictly outside the plane?  FP32 filter, FP64 certification within the margin.
-template <class T>
-__device__ __forceinline__ bool outside(const WarpState<T>& S, int s, const FPlane& f, const double4& pl, double tol) {
-    float4 v = S.fv[s];
-    float s32 = fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d;
-    if (fabsf(s32) > f.m) return s32 > 0.f;
-    return fma(pl.x, S.vx[s], fma(pl.y, S.vy[s], pl.z * S.vz[s])) - pl.w > tol;
-}
-
 // Clip the cell by {y : n.y <= d} (re-designed warp-parallel).
 template <class T>
 __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, double tol, FPlane f, int pidn) {
@@ -391,96 +405,129 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, 
         plane_gc(S, c, lane);
         if (c.np >= T::PMAX) return CLIP_OVF;
     }
+    // warp-uniform counts snapshotted in registers; published to the shared Cell only at the end,
+    // after a __syncwarp, so no lane can observe a half-updated cell
+    const int nv0 = c.nv, np0 = c.np;
     // 1. classify (outside <=> s > tol; on-plane vertices are kept)
     int R = 0;
-    const int nch = (c.nv + 31) >> 5;
+    const int nch = (nv0 + 31) >> 5;
+    Box6 box;  // AABB of the kept vertices, fused into the classification pass
+    box.reset();
     for (int ch = 0; ch < nch; ++ch) {
         int s = ch * 32 + lane;
-        bool out = s < c.nv && outside(S, s, f, pl, tol);
+        bool out = false;
+        if (s < nv0) {
+            float4 v = S.fv[s];
+            float s32 = fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d;
+            if (fabsf(s32) > f.m) out = s32 > 0.f;
+            else out = fma(pl.x, S.vx[s], fma(pl.y, S.vy[s], pl.z * S.vz[s])) - pl.w > tol;
+            if (!out) box.add(v);
+        }
         unsigned m = __ballot_sync(FULL, out);
         if (out) S.rem[R + __popc(m & lanemask_lt())] = (uint16_t)s;  // removed slots, ascending
         if (lane == 0) S.omask[ch] = m;
         R += __popc(m);
     }
     if (R == 0) return CLIP_NONE;
-    if (R == c.nv) return CLIP_EMPTY;
+    if (R == nv0) return CLIP_EMPTY;
     __syncwarp();
     // 2. hole boundary: edge x->y of a removed vertex is a boundary edge iff its reverse y->x is not
-    //    held by another removed vertex.  Small tiers: each removed vertex toggles the parity bit of
-    //    its 3 unordered edges {x,y}; interior edges are toggled twice.  Large tiers: pairwise scan.
-    if (T::EDGE_BITMAP) {
-        for (int r = lane; r < R; r += 32) {
-            auto t = S.vt[S.rem[r]];
-            int a = ta(t), b = tb(t), cc = tc(t);
-            int k0 = min(a, b) * T::PMAX + max(a, b), k1 = min(b, cc) * T::PMAX + max(b, cc),
-                k2 = min(cc, a) * T::PMAX + max(cc, a);
-            atomicXor(&S.ebits[k0 >> 5], 1u << (k0 & 31));
-            atomicXor(&S.ebits[k1 >> 5], 1u << (k1 & 31));
-            atomicXor(&S.ebits[k2 >> 5], 1u << (k2 & 31));
-        }
-        __syncwarp();
-    }
+    //    held by another removed vertex, i.e. iff the unordered edge {x,y} occurs once among the
+    //    removed vertices (an interior edge occurs exactly twice).  Up to 10 removed vertices: one
+    //    edge per lane and a single __match_any_sync; otherwise the pairwise scan below.
     int B = 0;
-    for (int r0 = 0; r0 < R; r0 += 32) {
-        int r = r0 + lane;
-        int nb = 0;
-        uint32_t e0 = 0, e1 = 0, e2 = 0;
-        if (r < R) {
+    if (PD_MATCH && 3 * R <= 32) {
+        const int r = lane / 3, e = lane - 3 * r;
+        const bool act = lane < 3 * R;
+        uint32_t key = 0xffff0000u | (uint32_t)lane;  // unique for idle lanes
+        uint32_t dir = 0;
+        if (act) {
             auto t = S.vt[S.rem[r]];
             int a = ta(t), b = tb(t), cc = tc(t);
-            bool f0 = false, f1 = false, f2 = false;
-            if (T::EDGE_BITMAP) {
+            int x = e == 0 ? a : (e == 1 ? b : cc);
+            int y = e == 0 ? b : (e == 1 ? cc : a);
+            key = (uint32_t)min(x, y) | ((uint32_t)max(x, y) << 16);
+            dir = (uint32_t)x | ((uint32_t)y << 16);
+        }
+        const unsigned same = __match_any_sync(FULL, key);  // every lane must execute it
+        const bool bnd = act && __popc(same) == 1;
+        const unsigned bm = __ballot_sync(FULL, bnd);
+        if (bnd) S.bnd[__popc(bm & lanemask_lt())] = dir;
+        B = __popc(bm);
+    } else {
+        if (T::EDGE_BITMAP) {
+            for (int r = lane; r < R; r += 32) {
+                auto t = S.vt[S.rem[r]];
+                int a = ta(t), b = tb(t), cc = tc(t);
                 int k0 = min(a, b) * T::PMAX + max(a, b), k1 = min(b, cc) * T::PMAX + max(b, cc),
                     k2 = min(cc, a) * T::PMAX + max(cc, a);
-                f0 = !((S.ebits[k0 >> 5] >> (k0 & 31)) & 1u);
-                f1 = !((S.ebits[k1 >> 5] >> (k1 & 31)) & 1u);
-                f2 = !((S.ebits[k2 >> 5] >> (k2 & 31)) & 1u);
-            } else {
-#pragma unroll 1
-                for (int k = 0; k < R; ++k) {
-                    auto u = S.vt[S.rem[k]];
-                    f0 |= has_edge(u, b, a);
-                    f1 |= has_edge(u, cc, b);
-                    f2 |= has_edge(u, a, cc);
-                }
+                atomicXor(&S.ebits[k0 >> 5], 1u << (k0 & 31));
+                atomicXor(&S.ebits[k1 >> 5], 1u << (k1 & 31));
+                atomicXor(&S.ebits[k2 >> 5], 1u << (k2 & 31));
             }
-            // compact the (up to 3) boundary edges without local-memory arrays
-            uint32_t ab = (uint32_t)a | ((uint32_t)b << 16), bc = (uint32_t)b | ((uint32_t)cc << 16),
-                     ca = (uint32_t)cc | ((uint32_t)a << 16);
-            if (!f0) { e0 = ab; nb = 1; }
-            if (!f1) { if (nb == 0) e0 = bc; else e1 = bc; nb++; }
-            if (!f2) { if (nb == 0) e0 = ca; else if (nb == 1) e1 = ca; else e2 = ca; nb++; }
+            __syncwarp();
         }
-        int inc = nb;
+        for (int r0 = 0; r0 < R; r0 += 32) {
+            int r = r0 + lane;
+            int nb = 0;
+            uint32_t e0 = 0, e1 = 0, e2 = 0;
+            if (r < R) {
+                auto t = S.vt[S.rem[r]];
+                int a = ta(t), b = tb(t), cc = tc(t);
+                bool f0 = false, f1 = false, f2 = false;
+                if (T::EDGE_BITMAP) {
+                    int k0 = min(a, b) * T::PMAX + max(a, b), k1 = min(b, cc) * T::PMAX + max(b, cc),
+                        k2 = min(cc, a) * T::PMAX + max(cc, a);
+                    f0 = !((S.ebits[k0 >> 5] >> (k0 & 31)) & 1u);
+                    f1 = !((S.ebits[k1 >> 5] >> (k1 & 31)) & 1u);
+                    f2 = !((S.ebits[k2 >> 5] >> (k2 & 31)) & 1u);
+                } else {
+#pragma unroll 1
+                    for (int k = 0; k < R; ++k) {
+                        auto u = S.vt[S.rem[k]];
+                        f0 |= has_edge(u, b, a);
+                        f1 |= has_edge(u, cc, b);
+                        f2 |= has_edge(u, a, cc);
+                    }
+                }
+                // compact the (up to 3) boundary edges without local-memory arrays
+                uint32_t ab = (uint32_t)a | ((uint32_t)b << 16), bc = (uint32_t)b | ((uint32_t)cc << 16),
+                         ca = (uint32_t)cc | ((uint32_t)a << 16);
+                if (!f0) { e0 = ab; nb = 1; }
+                if (!f1) { if (nb == 0) e0 = bc; else e1 = bc; nb++; }
+                if (!f2) { if (nb == 0) e0 = ca; else if (nb == 1) e1 = ca; else e2 = ca; nb++; }
+            }
+            int inc = nb;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int v = __shfl_up_sync(FULL, inc, o);
-            if (lane >= o) inc += v;
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(FULL, inc, o);
+                if (lane >= o) inc += v;
+            }
+            int tot = __shfl_sync(FULL, inc, 31);
+            int pos = B + inc - nb;
+            if (B + tot <= T::VMAX + 64) {
+                if (nb > 0) S.bnd[pos] = e0;
+                if (nb > 1) S.bnd[pos + 1] = e1;
+                if (nb > 2) S.bnd[pos + 2] = e2;
+            }
+            B += tot;
         }
-        int tot = __shfl_sync(FULL, inc, 31);
-        int pos = B + inc - nb;
-        if (B + tot <= T::VMAX + 64) {
-            if (nb > 0) S.bnd[pos] = e0;
-            if (nb > 1) S.bnd[pos + 1] = e1;
-            if (nb > 2) S.bnd[pos + 2] = e2;
+        if (T::EDGE_BITMAP) {  // restore the all-zero bitmap
+            __syncwarp();
+            for (int r = lane; r < R; r += 32) {
+                auto t = S.vt[S.rem[r]];
+                int a = ta(t), b = tb(t), cc = tc(t);
+                S.ebits[(min(a, b) * T::PMAX + max(a, b)) >> 5] = 0u;
+                S.ebits[(min(b, cc) * T::PMAX + max(b, cc)) >> 5] = 0u;
+                S.ebits[(min(cc, a) * T::PMAX + max(cc, a)) >> 5] = 0u;
+            }
+            __syncwarp();
         }
-        B += tot;
     }
-    if (T::EDGE_BITMAP) {  // restore the all-zero bitmap
-        __syncwarp();
-        for (int r = lane; r < R; r += 32) {
-            auto t = S.vt[S.rem[r]];
-            int a = ta(t), b = tb(t), cc = tc(t);
-            S.ebits[(min(a, b) * T::PMAX + max(a, b)) >> 5] = 0u;
-            S.ebits[(min(b, cc) * T::PMAX + max(b, cc)) >> 5] = 0u;
-            S.ebits[(min(cc, a) * T::PMAX + max(cc, a)) >> 5] = 0u;
-        }
-        __syncwarp();
-    }
-    int nvn = c.nv - R + B;
-    if (nvn > T::VMAX || B > T::VMAX + 64 || c.np + 1 > T::PMAX) return CLIP_OVF;
+    int nvn = nv0 - R + B;
+    if (nvn > T::VMAX || B > T::VMAX + 64 || np0 + 1 > T::PMAX) return CLIP_OVF;
     // 3. append the plane, create (h, x, y) for every boundary edge
-    int hs = c.np;
+    int hs = np0;
     if (lane == 0) {
         S.pl[hs] = pl;
         S.pid[hs] = pidn;
@@ -493,9 +540,10 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, 
             int x = be & 0xffff, y = be >> 16;
             double vx, vy, vz;
             solve3(pl, S.pl[x], S.pl[y], vx, vy, vz);
-            int slot = e < R ? S.rem[e] : c.nv + (e - R);
+            int slot = e < R ? S.rem[e] : nv0 + (e - R);
             put_vertex(S.fv, S.vx, S.vy, S.vz, slot, vx, vy, vz);
             S.vt[slot] = tpack<typename T::trip_t>(hs, x, y);
+            box.add(make_float4((float)vx, (float)vy, (float)vz, 0.f));
         }
     }
     // 4. if fewer vertices were created than removed, move kept vertices from the tail into holes
@@ -503,7 +551,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, 
         int moved = 0;
         for (int ch = nvn >> 5; ch < nch; ++ch) {
             int s = ch * 32 + lane;
-            bool mover = s >= nvn && s < c.nv && !((S.omask[ch] >> lane) & 1u);
+            bool mover = s >= nvn && s < nv0 && !((S.omask[ch] >> lane) & 1u);
             unsigned mm = __ballot_sync(FULL, mover);
             if (mover) {
                 int dst = S.rem[B + moved + __popc(mm & lanemask_lt())];
@@ -514,10 +562,11 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, 
             moved += __popc(mm);
         }
     }
-    c.nv = nvn;
+    c.nv = nvn;  // safe without a prior sync: no lane reads c.nv/c.np in clip after the snapshot
     c.np = hs + 1;
     __syncwarp();
-    update_aabb(S, c, lane);
+    if (PD_FUSED_AABB) finish_aabb(c, box);
+    else update_aabb(S, c, lane);
     return CLIP_DONE;
 }
 
@@ -646,7 +695,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
     bool have = true;
     int ns = 0;  // spilled entries
     const unsigned long long nodes0 = cnt.nodes;
-    c.nq = 0;
+    int nq = 0;  // queue length (warp-uniform register)
     for (;;) {
         if (have) {
             PT_BEGIN(t_desc);
@@ -686,19 +735,19 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 int npush = __popc(pm);
                 if (npush) {
                     int rank = __popc(pm & lanemask_lt());
-                    int room = T::QMAX - c.nq;
+                    int room = T::QMAX - nq;
                     int tos = max(npush - room, 0);
                     if (ns + tos > spill_cap) return ST_OVERFLOW;
                     if (push) {
                         if (rank < room) {
-                            S.qlo[c.nq + rank] = lo_w;
-                            S.qhi[c.nq + rank] = hi_l;
+                            S.qlo[nq + rank] = lo_w;
+                            S.qhi[nq + rank] = hi_l;
                         } else {
                             spill[ns + rank - room].lo_w = lo_w;
                             spill[ns + rank - room].hi_l = hi_l;
                         }
                     }
-                    c.nq += npush - tos;
+                    nq += npush - tos;
                     ns += tos;
                     cnt.spills += tos;
                 }
@@ -717,7 +766,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         // pop (Alg. 1 lines 21-31): re-validate every queued entry against the shrunk cell
         PT_BEGIN(t_pop);
         __syncwarp();
-        if (c.nq == 0 && ns > 0) {  // refill from the spill stack
+        if (nq == 0 && ns > 0) {  // refill from the spill stack
             __threadfence_block();
             int mm = min(ns, T::QMAX);
             for (int t = lane; t < mm; t += 32) {
@@ -726,18 +775,18 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 S.qhi[t] = e.hi_l;
             }
             ns -= mm;
-            c.nq = mm;
+            nq = mm;
             __syncwarp();
         }
-        if (c.nq == 0) return ST_OK;
+        if (nq == 0) return ST_OK;
         if (dfs) {
             bool ok = false;
-            while (c.nq > 0 && !ok) {
-                int t = c.nq - 1;
+            while (nq > 0 && !ok) {
+                int t = nq - 1;
                 bool culled;
                 node_test(c, S.qlo[t], S.qhi[t], flags, culled);
                 node = __float_as_int(S.qhi[t].w);
-                c.nq--;
+                nq--;
                 ok = !culled;
             }
             __syncwarp();
@@ -749,11 +798,11 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             continue;
         }
         int bestk = 0x7fffffff, bests = -1;
-        const int qch = (c.nq + 31) >> 5;
+        const int qch = (nq + 31) >> 5;
         for (int ch = 0; ch < qch; ++ch) {
             int s = ch * 32 + lane;
             bool al = false;
-            if (s < c.nq) {
+            if (s < nq) {
                 bool culled;
                 float k = node_test(c, S.qlo[s], S.qhi[s], flags, culled);
                 al = !culled;
@@ -765,7 +814,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         __syncwarp();
         int gk = __reduce_min_sync(FULL, bestk);
         if (gk == 0x7fffffff) {
-            c.nq = 0;
+            nq = 0;
             have = false;
             if (ns > 0) continue;
             return ST_OK;
@@ -793,7 +842,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             __syncwarp();
             base += __popc(km);
         }
-        c.nq = base;
+        nq = base;
         have = !popped_dead;
         PT_END(t_pop, 4);
     }
