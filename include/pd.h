@@ -151,6 +151,12 @@ pd_status pd_export_slice(const pd_result* r, int32_t* cnt, float* vol, float* s
                           void* stream);
 int64_t pd_slice_nnz(const pd_result* r);
 
+/* Test hook for the path's own LSD radix sort: stable sort of n (key < 2^64,
+ * value) pairs, all DEVICE pointers on the current device, enqueued on `stream` and synchronized.
+ * keys_in/vals_in are not modified; temp storage is allocated internally. */
+pd_status pd_sort_pairs_u64(const uint64_t* keys_in, const uint32_t* vals_in, int64_t n, uint64_t* keys_out,
+                            uint32_t* vals_out, void* stream);
+
 const char* pd_strerror(pd_status s);
 int64_t pd_error_index(void);      /* thread-local: offending point of the last NONFINITE/OUTSIDE */
 const char* pd_last_cuda_error(void); /* thread-local message of the last PD_ECUDA */

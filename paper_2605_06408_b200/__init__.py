@@ -27,7 +27,8 @@ CELL_EMPTY, CELL_BOUNDARY, CELL_OVERFLOW, CELL_DUPLICATE, CELL_NOT_OWNED = 1, 2,
 EXPORTED = ["pd_build", "pd_num_cells", "pd_nnz", "pd_on_host", "pd_offsets", "pd_neighbors", "pd_face_areas",
             "pd_volumes", "pd_surface", "pd_cell_flags", "pd_cell_cost", "pd_get_stats", "pd_free", "pd_slice_begin",
             "pd_slice_end", "pd_morton_perm", "pd_assemble", "pd_export_slice", "pd_slice_nnz",
-            "pd_strerror", "pd_error_index", "pd_last_cuda_error", "pd_abi_version", "pd_last_launch_count"]
+            "pd_strerror", "pd_error_index", "pd_last_cuda_error", "pd_abi_version", "pd_last_launch_count",
+            "pd_sort_pairs_u64"]
 
 
 class PdError(RuntimeError):
@@ -98,6 +99,9 @@ def load_library(path: str | None = None):
     L.pd_last_cuda_error.restype = ctypes.c_char_p
     L.pd_abi_version.restype = ctypes.c_int
     L.pd_last_launch_count.restype = I64
+    if hasattr(L, "pd_sort_pairs_u64"):  # optional test hook (absent in older A/B builds)
+        L.pd_sort_pairs_u64.restype = ctypes.c_int
+        L.pd_sort_pairs_u64.argtypes = [P, P, I64, P, P, P]
     _lib = L
     return L
 
@@ -280,6 +284,19 @@ def export_slice(d: Diagram, stream=None):
                              rn.data_ptr(), ra.data_ptr(), ctypes.byref(total), ctypes.c_void_p(stream)))
     t = int(total.value)
     return cnt, vol, surf, flg, rn[:t], ra[:t]
+
+
+def sort_pairs_u64(keys, vals, stream=None):
+    """pd_sort_pairs_u64 test hook: stable sort of int64 (non-negative) keys with int32 values (CUDA)."""
+    import torch
+    L = load_library()
+    ko = torch.empty_like(keys)
+    vo = torch.empty_like(vals)
+    if stream is None:
+        stream = torch.cuda.current_stream(keys.device).cuda_stream
+    _check(L.pd_sort_pairs_u64(keys.data_ptr(), vals.data_ptr(), keys.numel(), ko.data_ptr(), vo.data_ptr(),
+                               ctypes.c_void_p(stream)))
+    return ko, vo
 
 
 def cell_cost(d: Diagram):

@@ -575,6 +575,25 @@ pd_status pd_assemble(const int32_t* perm, const int32_t* cnt_m, const float* vo
     }
 }
 
+pd_status pd_sort_pairs_u64(const uint64_t* keys_in, const uint32_t* vals_in, int64_t n, uint64_t* keys_out,
+                            uint32_t* vals_out, void* stream) {
+    if (n < 0 || (n > 0 && (!keys_in || !vals_in || !keys_out || !vals_out))) return PD_EINVAL;
+    if (n == 0) return PD_OK;
+    try {
+        cudaStream_t st = (cudaStream_t)stream;
+        Arena A(st);
+        size_t tb = 0;
+        ck(pd::sort_pairs(keys_in, keys_out, vals_in, vals_out, n, nullptr, &tb, st, nullptr));
+        void* tmp = A.alloc<unsigned char>(tb);
+        int launches = 0;
+        ck(pd::sort_pairs(keys_in, keys_out, vals_in, vals_out, n, tmp, &tb, st, &launches));
+        ck(cudaStreamSynchronize(st));
+        return PD_OK;
+    } catch (const Fail& f) {
+        return f.s;
+    }
+}
+
 const char* pd_strerror(pd_status s) {
     switch (s) {
         case PD_OK: return "ok";

@@ -1,6 +1,5 @@
-// pd_csr.cu -- a4 radix sort and a13 CSR compaction (device prefix scan + row gather), plus the
+// pd_csr.cu -- a13 CSR compaction (row gather after the device prefix scan of pd_sort.cu), plus the
 // Morton-order slice export / reassembly used by the sharded (multi-GPU) build.
-#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -10,10 +9,6 @@ namespace pd {
 namespace {
 
 inline unsigned blocks(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
-
-struct ToI64 {
-    __host__ __device__ int64_t operator()(int32_t v) const { return (int64_t)v; }
-};
 
 // One warp per 32 rows: lanes cooperate on each row so the copies are coalesced.
 __global__ void k_csr_gather(const int32_t* __restrict__ cnt, const int64_t* __restrict__ aoff,
@@ -95,23 +90,6 @@ __global__ void k_fill_u8(uint8_t* p, int64_t n, uint8_t v) {
 }
 
 }  // namespace
-
-cudaError_t sort_pairs(const uint64_t* keys_in, uint64_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
-                       int64_t n, void* temp, size_t* temp_bytes, cudaStream_t st, int* launches) {
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(temp, *temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)n, 0, 63, st);
-    if (temp && launches) *launches += 8;  // onesweep: histogram + passes
-    return e;
-}
-
-cudaError_t scan_counts(const int32_t* cnt, int64_t* offsets, int64_t n, void* temp, size_t* temp_bytes,
-                        cudaStream_t st, int* launches) {
-    cub::TransformInputIterator<int64_t, ToI64, const int32_t*> it(cnt, ToI64());
-    if (temp) {
-        cudaMemsetAsync(offsets, 0, sizeof(int64_t), st);
-        if (launches) *launches += 2;
-    }
-    return cub::DeviceScan::InclusiveSum(temp, *temp_bytes, it, offsets + 1, (int)n, st);
-}
 
 cudaError_t csr_gather(const int32_t* cnt, const int64_t* aoff, const int64_t* offsets, const int32_t* arena_nbr,
                        const float* arena_area, int64_t n, int32_t* nbr, float* area, cudaStream_t st, int* launches) {

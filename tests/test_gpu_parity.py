@@ -186,6 +186,17 @@ def test_sharded_reassembly_matches_single():
             assert np.array_equal(getattr(ref, k), getattr(full, k)), (world, k)
 
 
+@pytest.mark.parametrize("n,bits", [(1, 62), (1000, 8), (4096 * 3 + 17, 62), (1_000_003, 62), (2_000_000, 20)])
+def test_own_radix_sort_matches_stable_torch_sort(n, bits):
+    """a4: the path's own LSD radix sort equals a stable sort (ties keep input order)."""
+    g = torch.Generator().manual_seed(n)
+    keys = torch.randint(0, 2 ** bits, (n,), generator=g, dtype=torch.int64).cuda()
+    vals = torch.arange(n, dtype=torch.int32).cuda()
+    ko, vo = pd.sort_pairs_u64(keys, vals)
+    ref_k, ref_i = torch.sort(keys, stable=True)
+    assert torch.equal(ko, ref_k) and torch.equal(vo, ref_i.to(torch.int32))
+
+
 # ----------------------------------------------------------------- full sizes, sampled cells
 
 FULL = [("C2", 256), ("C3", 128), ("C4", 96), ("C5", 64)]
