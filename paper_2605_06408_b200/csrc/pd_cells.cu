@@ -36,6 +36,9 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef PD_BATCH_CUT
+#define PD_BATCH_CUT 0
+#endif
 #ifndef PD_MATCH
 #define PD_MATCH 1
 #endif
@@ -401,13 +404,9 @@ __device__ __forceinline__ void solve3(double4 a, double4 b, double4 c, double& 
 // Clip the cell by {y : n.y <= d} (re-designed warp-parallel).
 template <class T>
 __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, double tol, FPlane f, int pidn) {
-    if (c.np >= (T::PMAX * 85) / 100) {
-        plane_gc(S, c, lane);
-        if (c.np >= T::PMAX) return CLIP_OVF;
-    }
     // warp-uniform counts snapshotted in registers; published to the shared Cell only at the end,
     // after a __syncwarp, so no lane can observe a half-updated cell
-    const int nv0 = c.nv, np0 = c.np;
+    const int nv0 = c.nv;
     // 1. classify (outside <=> s > tol; on-plane vertices are kept)
     int R = 0;
     const int nch = (nv0 + 31) >> 5;
@@ -431,6 +430,12 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, 
     if (R == 0) return CLIP_NONE;
     if (R == nv0) return CLIP_EMPTY;
     __syncwarp();
+    int np0 = c.np;
+    if (np0 >= (T::PMAX * 85) / 100) {  // plane garbage collection (vertex slots are unaffected)
+        plane_gc(S, c, lane);
+        np0 = c.np;
+        if (np0 >= T::PMAX) return CLIP_OVF;
+    }
     // 2. hole boundary: edge x->y of a removed vertex is a boundary edge iff its reverse y->x is not
     //    held by another removed vertex, i.e. iff the unordered edge {x,y} occurs once among the
     //    removed vertices (an interior edge occurs exactly twice).  Up to 10 removed vertices: one
@@ -635,7 +640,7 @@ __device__ PD_INL_LEAF int process_leaf(WarpState<T>& S, Cell& c, int lane, int 
     // predicate as clip().
     const float dd = 0.5f * (D2 + dq);
     const float m = 1e-6f * ((fabsf(Dx) + fabsf(Dy) + fabsf(Dz)) * c.vmax + D2 + fabsf(dq));
-    {
+    if (PD_BATCH_CUT) {
         bool cuts = false, amb = false;
         if (cand) {
 #pragma unroll 4
@@ -651,6 +656,7 @@ __device__ PD_INL_LEAF int process_leaf(WarpState<T>& S, Cell& c, int lane, int 
         cand = cand && cuts;
         mask = __ballot_sync(FULL, cand);
     }
+    if (!PD_BATCH_CUT) cnt.tests += __popc(mask);
     float key = cand ? dd * rsqrtf(D2) : INFINITY;  // d_ij: nearest plane first
     while (mask) {
         int kmin = __reduce_min_sync(FULL, cand ? ford(key) : 0x7fffffff);
