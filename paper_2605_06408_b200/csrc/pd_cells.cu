@@ -36,6 +36,9 @@ namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef PD_LAZY_POP
+#define PD_LAZY_POP 0
+#endif
 #ifndef PD_BATCH_CUT
 #define PD_BATCH_CUT 0
 #endif
@@ -86,7 +89,10 @@ struct TierCfg {
 #ifndef PD_T1_V
 #define PD_T1_V 96
 #endif
-using Tier1 = TierCfg<PD_T1_V, 64, PD_T1_Q, 4, PD_T1_MINB>;
+#ifndef PD_T1_P
+#define PD_T1_P 64
+#endif
+using Tier1 = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, 4, PD_T1_MINB>;
 using Tier2 = TierCfg<384, 192, 256, 4, 1>;
 // Top tier: state in global memory (L1/L2-cached), 64-bit plane-index triplets; for the rare cells
 // with thousands of faces (heavy-tailed weights, SURVEY.md §7 hard part 3).
@@ -119,6 +125,7 @@ struct __align__(16) WarpState {
         struct {                  // traversal: priority queue of pushed child records
             float4 qlo[T::QMAX];  // (lo, maxw)
             float4 qhi[T::QMAX];  // (hi, link)
+            float qkey[PD_LAZY_POP ? T::QMAX : 1];  // priority at push time (lazy pop only)
         };
         struct {                  // finalize (the queue is dead by then)
             uint16_t tw[3][T::VMAX];  // twin vertex across edges a->b, b->c, c->a
@@ -130,7 +137,7 @@ struct __align__(16) WarpState {
     uint16_t rem[T::VMAX];        // removed-vertex slots of the current clip
     uint32_t omask[T::VC];        // outside-vertex ballots of the current clip
     uint32_t qmask[T::QC];        // alive-entry ballots of the current pop
-    uint32_t bnd[T::VMAX + 64];   // boundary edges (x | y << 16) of the current clip
+    uint32_t bnd[T::VMAX];        // boundary edges (x | y << 16) of the current clip (B <= VMAX unless overflow)
     uint16_t pmap[T::PMAX];       // plane GC remap
     uint32_t ebits[T::EBW];       // hole-edge parity bitmap (zero between clips)
 };
@@ -510,7 +517,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, 
             }
             int tot = __shfl_sync(FULL, inc, 31);
             int pos = B + inc - nb;
-            if (B + tot <= T::VMAX + 64) {
+            if (B + tot <= T::VMAX) {
                 if (nb > 0) S.bnd[pos] = e0;
                 if (nb > 1) S.bnd[pos + 1] = e1;
                 if (nb > 2) S.bnd[pos + 2] = e2;
@@ -530,7 +537,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, 
         }
     }
     int nvn = nv0 - R + B;
-    if (nvn > T::VMAX || B > T::VMAX + 64 || np0 + 1 > T::PMAX) return CLIP_OVF;
+    if (nvn > T::VMAX || B > T::VMAX || np0 + 1 > T::PMAX) return CLIP_OVF;
     // 3. append the plane, create (h, x, y) for every boundary edge
     int hs = np0;
     if (lane == 0) {
@@ -746,6 +753,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     if (ns + tos > spill_cap) return ST_OVERFLOW;
                     if (push) {
                         if (rank < room) {
+                            if (PD_LAZY_POP) S.qkey[nq + rank] = key;
                             S.qlo[nq + rank] = lo_w;
                             S.qhi[nq + rank] = hi_l;
                         } else {
@@ -777,6 +785,10 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             int mm = min(ns, T::QMAX);
             for (int t = lane; t < mm; t += 32) {
                 NodeChild e = spill[ns - mm + t];
+                if (PD_LAZY_POP) {
+                    bool cu;
+                    S.qkey[t] = node_test(c, e.lo_w, e.hi_l, flags, cu);
+                }
                 S.qlo[t] = e.lo_w;
                 S.qhi[t] = e.hi_l;
             }
@@ -801,6 +813,35 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 return ST_OK;
             }
             have = true;
+            continue;
+        }
+        if (PD_LAZY_POP) {
+            // the paper's unsorted-queue pop: min over the push-time priorities,
+            // re-validate only the popped entry (Alg. 1 lines 25-29), fill its hole with the last one
+            int bk = 0x7fffffff, bs = -1;
+            for (int s = lane; s < nq; s += 32) {
+                int k = ford(S.qkey[s]);
+                if (k < bk) { bk = k; bs = s; }
+            }
+            int gk = __reduce_min_sync(FULL, bk);
+            int bslot = __shfl_sync(FULL, bs, __ffs(__ballot_sync(FULL, bk == gk)) - 1);
+            float4 lo = S.qlo[bslot], hi = S.qhi[bslot];
+            __syncwarp();
+            if (lane == 0 && bslot != nq - 1) {
+                S.qlo[bslot] = S.qlo[nq - 1];
+                S.qhi[bslot] = S.qhi[nq - 1];
+                S.qkey[bslot] = S.qkey[nq - 1];
+            }
+            --nq;
+            __syncwarp();
+            bool culled;
+            node_test(c, lo, hi, flags, culled);
+            if (!culled && (exact_on(flags, cnt.nodes - nodes0, P.exact_after) ||
+                            (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) && __float_as_int(hi.w) < 0)))
+                culled = node_exact_culled(S, c, lane, lo, hi);
+            node = __float_as_int(hi.w);
+            have = !culled;
+            PT_END(t_pop, 4);
             continue;
         }
         int bestk = 0x7fffffff, bests = -1;
