@@ -409,8 +409,16 @@ __device__ __forceinline__ void solve3(double4 a, double4 b, double4 c, double& 
 }
 
 // Clip the cell by {y : n.y <= d} (re-designed warp-parallel).
+__device__ __forceinline__ double4 exact_plane(const Cell& c, float4 sj) {
+    // the exact FP64 plane of candidate site sj: n = p_j - p_i, d = (|n|^2 + w_i - w_j)/2
+    double ex = (double)sj.x - c.px, ey = (double)sj.y - c.py, ez = (double)sj.z - c.pz;
+    return make_double4(ex, ey, ez, 0.5 * (ex * ex + ey * ey + ez * ez + (c.pw - (double)sj.w)));
+}
+
 template <class T>
-__device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, double tol, FPlane f, int pidn) {
+__device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, FPlane f, int pidn) {
+    // FP64 tolerance for certification (only evaluated on ambiguous classifications)
+    const double tol = 1e-12 * (double)sqrtf(f.nx * f.nx + f.ny * f.ny + f.nz * f.nz) * (double)c.rmax;
     // warp-uniform counts snapshotted in registers; published to the shared Cell only at the end,
     // after a __syncwarp, so no lane can observe a half-updated cell
     const int nv0 = c.nv;
@@ -426,7 +434,10 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, 
             float4 v = S.fv[s];
             float s32 = fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d;
             if (fabsf(s32) > f.m) out = s32 > 0.f;
-            else out = fma(pl.x, S.vx[s], fma(pl.y, S.vy[s], pl.z * S.vz[s])) - pl.w > tol;
+            else {
+                const double4 pe = exact_plane(c, sj);
+                out = fma(pe.x, S.vx[s], fma(pe.y, S.vy[s], pe.z * S.vz[s])) - pe.w > tol;
+            }
             if (!out) box.add(v);
         }
         unsigned m = __ballot_sync(FULL, out);
@@ -437,6 +448,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, double4 pl, 
     if (R == 0) return CLIP_NONE;
     if (R == nv0) return CLIP_EMPTY;
     __syncwarp();
+    const double4 pl = exact_plane(c, sj);
     int np0 = c.np;
     if (np0 >= (T::PMAX * 85) / 100) {  // plane garbage collection (vertex slots are unaffected)
         plane_gc(S, c, lane);
@@ -672,18 +684,13 @@ __device__ PD_INL_LEAF int process_leaf(WarpState<T>& S, Cell& c, int lane, int 
         float sx = __shfl_sync(FULL, sj.x, src), sy = __shfl_sync(FULL, sj.y, src), sz = __shfl_sync(FULL, sj.z, src),
               sw = __shfl_sync(FULL, sj.w, src);
         if (lane == src) cand = false;
-        // the exact plane of the selected candidate, recomputed identically on every lane
-        double ex = (double)sx - c.px, ey = (double)sy - c.py, ez = (double)sz - c.pz;
-        double e2 = ex * ex + ey * ey + ez * ez;
-        double4 pl = make_double4(ex, ey, ez, 0.5 * (e2 + (c.pw - (double)sw)));
-        double tol = 1e-12 * (double)sqrtf((float)e2) * (double)c.rmax;
         FPlane f;
         f.nx = sx - c.fpx; f.ny = sy - c.fpy; f.nz = sz - c.fpz;
         float f2 = f.nx * f.nx + f.ny * f.ny + f.nz * f.nz, fdq = c.fpw - sw;
         f.d = 0.5f * (f2 + fdq);
         f.m = 1e-6f * ((fabsf(f.nx) + fabsf(f.ny) + fabsf(f.nz)) * c.vmax + f2 + fabsf(fdq));
         PT_BEGIN(t_clip);
-        int st = clip(S, c, lane, pl, tol, f, first + src);
+        int st = clip(S, c, lane, make_float4(sx, sy, sz, sw), f, first + src);
         PT_END(t_clip, 3);
         if (st == CLIP_EMPTY) return ST_EMPTY;
         if (st == CLIP_OVF) return ST_OVERFLOW;
