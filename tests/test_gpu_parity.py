@@ -56,6 +56,37 @@ def test_configs_full_small(cfg, n):
     _assert_parity(pdgen.make(cfg, n=n))
 
 
+def _paper_workload(kind, n, seed, weighted):
+    """The paper's synthetic laws: white noise, K Gaussian clusters (sigma=0.1),
+    linear density gradient; optionally w ~ N(0, (d_nn^2/3)^2)."""
+    if kind == "white":
+        p = pdgen.white_noise(n, seed)
+    elif kind.startswith("clustered"):
+        p = pdgen.clustered(n, seed, k=int(kind[9:]), sigma=0.1)
+    else:
+        p = pdgen.density_gradient(n, seed)
+    w = pdgen.weights_paper(n, pdgen.median_nn_distance(p), seed) if weighted else None
+    return pdgen.Workload(f"{kind}{'-w' if weighted else ''}", p, w, pdgen.OMEGA_BOX, kind)
+
+
+@pytest.mark.parametrize("kind", ["white", "clustered5", "clustered10", "gradient"])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_paper_workloads(kind, weighted):
+    _assert_parity(_paper_workload(kind, 12007, 21, weighted))
+
+
+@pytest.mark.parametrize("ratio", [0.0, 1.0, 10.0, 100.0])
+def test_weight_magnitude_sweep(ratio):
+    """Weight-magnitude sweep (PAPER.md:563-581 analogue): larger weights empty
+    more cells; the diagram stays exact."""
+    p = pdgen.white_noise(8009, 5)
+    d = pdgen.median_nn_distance(p)
+    w = pdgen.weights_paper(8009, d, 5, ratio=ratio)
+    g, o, rep = _assert_parity(pdgen.Workload(f"sweep{ratio}", p, w, pdgen.OMEGA_BOX, ""))
+    if ratio >= 10:
+        assert np.mean(g.flags & pd.CELL_EMPTY) > 0.05
+
+
 @pytest.mark.parametrize("leaf", [1, 7, 16, 32])
 def test_leaf_sizes_identical(leaf):
     wl = pdgen.make("C5", n=5003)
