@@ -61,7 +61,8 @@ enum {
     PD_PAPER_BOUND = 1u << 6, /* ablation: the paper's culling bounds only (no AABB-support companion) */
     PD_COST = 1u << 7,        /* record per-cell work (pd_cell_cost): BVH nodes + leaf sites + clips */
     PD_EXACT_NODES = 1u << 8, /* exact polytope-vs-box node test on every node the AABB tests keep */
-    PD_NO_EXACT = 1u << 9     /* never use the exact polytope-vs-box node test (pure AABB culling) */
+    PD_NO_EXACT = 1u << 9,    /* never use the exact polytope-vs-box node test (pure AABB culling) */
+    PD_NO_BALANCE = 1u << 10  /* sharded build: equal-count Morton slices instead of equal-cost ones */
 };
 
 /* pd_cell_flags values */

@@ -21,7 +21,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpd.so")
 
 PD_OK, PD_EINVAL, PD_EEMPTY, PD_ENONFINITE, PD_EOUTSIDE, PD_ENOMEM, PD_ECUDA, PD_ENCCL, PD_EINTERNAL = range(9)
-IN_DEVICE, OUT_HOST, STATS, ISOTROPIC, DFS, PAPER_BOUND, COST, EXACT_NODES, NO_EXACT = 1, 2, 4, 8, 16, 64, 128, 256, 512
+IN_DEVICE, OUT_HOST, STATS, ISOTROPIC, DFS, PAPER_BOUND, COST, EXACT_NODES, NO_EXACT, NO_BALANCE = (
+    1, 2, 4, 8, 16, 64, 128, 256, 512, 1024)
 CELL_EMPTY, CELL_BOUNDARY, CELL_OVERFLOW, CELL_DUPLICATE, CELL_NOT_OWNED = 1, 2, 4, 8, 32
 
 EXPORTED = ["pd_build", "pd_num_cells", "pd_nnz", "pd_on_host", "pd_offsets", "pd_neighbors", "pd_face_areas",

@@ -330,14 +330,88 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         ck(pd::bvh_topology(keys_s, sorted, (int)n, leaf, sc, bvh, st, &launches));
         ck(cudaEventRecord(ev[1], st));
         // ---- cells
-        int64_t begin = (n * rank) / world, end = (n * (rank + 1)) / world;
-        r->slice_begin = begin;
-        r->slice_end = end;
         int32_t* cnt = A.alloc<int32_t>(n);
         int64_t* aoff = W.alloc<int64_t>(n);
         float* vol = A.alloc<float>(n);
         float* surf = A.alloc<float>(n);
         uint8_t* flags = A.alloc<uint8_t>(n);
+        int sms = num_sms(opt.device);
+        const int spill_cap[3] = {2048, 8192, 32768};
+        size_t spill_entries = 0;
+        for (int t = 0; t < 3; ++t)
+            spill_entries = std::max(spill_entries, (size_t)pd::cells_grid_warps(t, sms) * spill_cap[t]);
+        pd::NodeChild* spill = W.alloc<pd::NodeChild>(spill_entries);
+        void* gstate = W.alloc<unsigned char>(pd::cells_global_state_bytes(sms));
+        const int exact_after = [] {
+            const char* ev = getenv("PD_EXACT_AFTER");  // tuning knob (default 200)
+            return ev ? atoi(ev) : 200;
+        }();
+        // ---- slice of the Morton order owned by this rank: equal cost, estimated by
+        // running the tier-1 kernel with cost counters on a strided ~40k-cell sample (deterministic, so
+        // every rank computes the same cuts); PD_NO_BALANCE gives equal-count slices.
+        int64_t begin = (n * rank) / world, end = (n * (rank + 1)) / world;
+        if (world > 1 && !(opt.flags & PD_NO_BALANCE) && n >= 4 * world) {
+            const int64_t stride = std::max<int64_t>(1, n / 40000);
+            const int64_t ns = (n + stride - 1) / stride;
+            std::vector<int32_t> hpos(ns);
+            for (int64_t k = 0; k < ns; ++k) hpos[k] = (int32_t)(k * stride);
+            int32_t* spos = W.alloc<int32_t>(ns);
+            int32_t* scount = W.alloc<int32_t>(4);
+            int32_t* scost = W.alloc<int32_t>(n);
+            int32_t* sgath = W.alloc<int32_t>(ns);
+            unsigned long long* sctr = W.alloc<unsigned long long>(8);
+            const int64_t scap = ns * 96 + 4096;
+            int32_t* s_nbr = W.alloc<int32_t>(scap);
+            float* s_area = W.alloc<float>(scap);
+            int* s_ovf = W.alloc<int>(1);
+            pd::Stats* s_stats = W.alloc<pd::Stats>(1);
+            int32_t* s_next = W.alloc<int32_t>(ns);
+            int32_t hc[4] = {(int32_t)ns, 0, 0, 0};
+            ck(cudaMemcpyAsync(spos, hpos.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, st));
+            ck(cudaMemcpyAsync(scount, hc, sizeof(hc), cudaMemcpyHostToDevice, st));
+            ck(cudaMemsetAsync(sctr, 0, 8 * sizeof(unsigned long long), st));
+            ck(cudaMemsetAsync(s_ovf, 0, sizeof(int), st));
+            pd::CellParams Q;
+            memset(&Q, 0, sizeof(Q));
+            Q.sites = sorted;
+            Q.perm = perm;
+            Q.nodes = bvh.nodes;
+            Q.root = bvh.root;
+            for (int k = 0; k < 3; ++k) { Q.box_lo[k] = hbox[k]; Q.box_hi[k] = hbox[3 + k]; }
+            Q.flags = (opt.flags | PD_COST) & ~PD_STATS;
+            Q.out.cnt = cnt; Q.out.aoff = aoff; Q.out.vol = vol; Q.out.surf = surf; Q.out.flags = flags;
+            Q.out.arena_nbr = s_nbr; Q.out.arena_area = s_area; Q.out.arena_top = sctr + 4;
+            Q.out.arena_cap = scap; Q.out.arena_overflow = s_ovf; Q.out.cost = scost;
+            Q.stats = s_stats;
+            Q.spill = spill;
+            Q.gstate = gstate;
+            Q.exact_after = exact_after;
+            Q.work_counter = sctr;
+            Q.last_tier = 1;  // heavy sampled cells keep their (partial) cost instead of escalating
+            Q.list = spos;
+            Q.list_count = scount;
+            Q.next_list = s_next;
+            Q.next_count = scount + 1;
+            Q.spill_cap = spill_cap[0];
+            ck(pd::launch_cells(0, Q, st, sms, &launches));
+            ck(pd::gather_sample_cost(perm, spos, ns, scost, sgath, st, &launches));
+            std::vector<int32_t> hcost(ns);
+            ck(cudaMemcpyAsync(hcost.data(), sgath, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, st));
+            ck(cudaStreamSynchronize(st));
+            std::vector<double> cum(ns + 1, 0.0);
+            for (int64_t k = 0; k < ns; ++k) cum[k + 1] = cum[k] + std::max<int32_t>(hcost[k], 1);
+            auto cut = [&](int q) -> int64_t {  // Morton position where cumulative cost reaches q/world
+                if (q <= 0) return 0;
+                if (q >= world) return n;
+                const double target = cum[ns] * q / world;
+                int64_t k = std::lower_bound(cum.begin(), cum.end(), target) - cum.begin();
+                return std::min<int64_t>(n, std::max<int64_t>(0, (k - 1) * stride));
+            };
+            begin = cut(rank);
+            end = cut(rank + 1);
+        }
+        r->slice_begin = begin;
+        r->slice_end = end;
         int32_t* lists = W.alloc<int32_t>(2 * (size_t)std::max<int64_t>(end - begin, 1));
         unsigned long long* counters = W.alloc<unsigned long long>(8);
         int32_t* list_counts = W.alloc<int32_t>(4);
@@ -350,13 +424,6 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         int32_t* nbr = nullptr;  // CSR outputs: allocated with the arena (same capacity) so the CSR
         float* area = nullptr;   // phase never grows the memory pool mid-build
         float* aarea = nullptr;
-        int sms = num_sms(opt.device);
-        const int spill_cap[3] = {2048, 8192, 32768};
-        size_t spill_entries = 0;
-        for (int t = 0; t < 3; ++t)
-            spill_entries = std::max(spill_entries, (size_t)pd::cells_grid_warps(t, sms) * spill_cap[t]);
-        pd::NodeChild* spill = W.alloc<pd::NodeChild>(spill_entries);
-        void* gstate = W.alloc<unsigned char>(pd::cells_global_state_bytes(sms));
         cudaEvent_t tev[4];
         for (auto& e : tev) ck(cudaEventCreate(&e));
         for (int attempt = 0; attempt < 3; ++attempt) {
@@ -396,10 +463,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.stats = dstats;
             P.spill = spill;
             P.gstate = gstate;
-            {
-                const char* ev = getenv("PD_EXACT_AFTER");  // tuning knob (default 200)
-                P.exact_after = ev ? atoi(ev) : 200;
-            }
+            P.exact_after = exact_after;
             int64_t L = end - begin;
             for (int tier = 0; tier < 3; ++tier) {
                 P.work_counter = counters + tier;

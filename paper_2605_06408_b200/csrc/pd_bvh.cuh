@@ -55,5 +55,8 @@ cudaError_t assemble_rows(const int32_t* perm, int64_t n, const int32_t* cnt_m, 
                           const int64_t* offsets, const int32_t* rows_nbr, const float* rows_area, int32_t* nbr,
                           float* area, cudaStream_t st, int* launches);
 cudaError_t fill_flags(uint8_t* flags, int64_t n, uint8_t v, cudaStream_t st, int* launches);
+// out[k] = cost[perm[pos[k]]] for the sampled Morton positions (cost-balanced slicing)
+cudaError_t gather_sample_cost(const int32_t* perm, const int32_t* pos, int64_t ns, const int32_t* cost, int32_t* out,
+                               cudaStream_t st, int* launches);
 
 }  // namespace pd

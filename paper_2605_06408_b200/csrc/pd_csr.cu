@@ -89,7 +89,20 @@ __global__ void k_fill_u8(uint8_t* p, int64_t n, uint8_t v) {
     if (k < n) p[k] = v;
 }
 
+__global__ void k_gather_cost(const int32_t* __restrict__ perm, const int32_t* __restrict__ pos, int64_t ns,
+                              const int32_t* __restrict__ cost, int32_t* __restrict__ out) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k < ns) out[k] = cost[perm[pos[k]]];
+}
+
 }  // namespace
+
+cudaError_t gather_sample_cost(const int32_t* perm, const int32_t* pos, int64_t ns, const int32_t* cost, int32_t* out,
+                               cudaStream_t st, int* launches) {
+    k_gather_cost<<<blocks(ns, 256), 256, 0, st>>>(perm, pos, ns, cost, out);
+    ++*launches;
+    return cudaGetLastError();
+}
 
 cudaError_t csr_gather(const int32_t* cnt, const int64_t* aoff, const int64_t* offsets, const int32_t* arena_nbr,
                        const float* arena_area, int64_t n, int32_t* nbr, float* area, cudaStream_t st, int* launches) {

@@ -203,14 +203,19 @@ def test_sharded_reassembly_matches_single():
     ref = _gpu(wl)
     p = torch.from_numpy(wl.points).cuda()
     w = torch.from_numpy(wl.weights).cuda()
-    for world in (2, 3):
+    for world, fl in ((2, 0), (3, 0), (3, pd.NO_BALANCE)):
         parts = []
         perm = None
+        bounds = []
         for r in range(world):
-            d = pd.build_diagram(p, w, wl.box, shard_rank=r, shard_world=world)
+            d = pd.build_diagram(p, w, wl.box, shard_rank=r, shard_world=world, flags=fl)
+            bounds.append((d.slice_begin, d.slice_end))
             parts.append(pd.export_slice(d))
             if perm is None:
                 perm = pd.morton_perm(d).clone()
+        # slices tile the Morton order (equal-cost cuts by default, equal-count with NO_BALANCE)
+        assert bounds[0][0] == 0 and bounds[-1][1] == wl.n
+        assert all(bounds[r][1] == bounds[r + 1][0] for r in range(world - 1))
         cat = [torch.cat([pp[k] for pp in parts]) for k in range(6)]
         full = pd.assemble(perm, *cat).to_numpy()
         for k in ("offsets", "neighbors", "areas", "volumes", "surface", "flags"):
