@@ -386,6 +386,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             Q.spill = spill;
             Q.gstate = gstate;
             Q.exact_after = exact_after;
+            Q.prof_tier = -2;
             Q.work_counter = sctr;
             Q.last_tier = 1;  // heavy sampled cells keep their (partial) cost instead of escalating
             Q.list = spos;
@@ -464,6 +465,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.spill = spill;
             P.gstate = gstate;
             P.exact_after = exact_after;
+            P.prof_tier = getenv("PD_PROF_TIER") ? atoi(getenv("PD_PROF_TIER")) : -1;
             int64_t L = end - begin;
             for (int tier = 0; tier < 3; ++tier) {
                 P.work_counter = counters + tier;

@@ -1105,7 +1105,8 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
         red_add_g(&P.stats->tier[tier], ncells);
         red_add_g(&P.stats->overflow, novf);
         red_add_g(&P.stats->spills, cnt.spills);
-        for (int k = 0; k < 6; ++k) red_add_g(&P.stats->cyc[k], cnt.cyc[k]);
+        if (P.prof_tier < 0 || P.prof_tier == tier)
+            for (int k = 0; k < 6; ++k) red_add_g(&P.stats->cyc[k], cnt.cyc[k]);
     }
 }
 

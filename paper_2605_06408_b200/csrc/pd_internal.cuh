@@ -76,6 +76,7 @@ struct CellParams {
     int spill_cap;      // entries per warp
     int exact_after;    // exact node tests once a cell has visited this many nodes
     void* gstate;       // top tier: per-warp cell state in global memory
+    int prof_tier;      // PD_PROFILE builds: tier whose phase cycles are recorded (-1 = all)
 };
 
 cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches);
