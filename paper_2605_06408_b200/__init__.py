@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpd.so")
 
 PD_OK, PD_EINVAL, PD_EEMPTY, PD_ENONFINITE, PD_EOUTSIDE, PD_ENOMEM, PD_ECUDA, PD_ENCCL, PD_EINTERNAL = range(9)
-IN_DEVICE, OUT_HOST, STATS, ISOTROPIC, DFS, PAPER_BOUND, COST, EXACT_NODES, NO_EXACT, NO_BALANCE = (
+IN_DEVICE, OUT_HOST, STATS, ISOTROPIC, DFS, PAPER_BOUND, COST, EXACT_NODES, NO_EXACT, BALANCE = (
     1, 2, 4, 8, 16, 64, 128, 256, 512, 1024)
 CELL_EMPTY, CELL_BOUNDARY, CELL_OVERFLOW, CELL_DUPLICATE, CELL_NOT_OWNED = 1, 2, 4, 8, 32
 
@@ -55,7 +55,7 @@ class Stats(ctypes.Structure):
                 ("nnz", ctypes.c_int64),
                 ("ms_bvh", ctypes.c_double), ("ms_cells", ctypes.c_double), ("ms_csr", ctypes.c_double),
                 ("ms_total", ctypes.c_double), ("ms_tier", ctypes.c_double * 3),
-                ("warp_cycles", ctypes.c_int64 * 6)]
+                ("warp_cycles", ctypes.c_int64 * 10)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}

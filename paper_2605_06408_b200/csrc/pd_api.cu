@@ -346,11 +346,12 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             const char* ev = getenv("PD_EXACT_AFTER");  // tuning knob (default 200)
             return ev ? atoi(ev) : 200;
         }();
-        // ---- slice of the Morton order owned by this rank: equal cost, estimated by
-        // running the tier-1 kernel with cost counters on a strided ~40k-cell sample (deterministic, so
-        // every rank computes the same cuts); PD_NO_BALANCE gives equal-count slices.
+        // ---- slice of the Morton order owned by this rank: equal-count by default;
+        // PD_BALANCE cuts equal estimated cost, from the tier-1 kernel's per-cell warp time on a strided
+        // ~40k-cell sample (deterministic, so every rank computes the same cuts).  Measured on C4 at
+        // world 8 (tools/shard_balance.py): equal-count max/mean 1.07, cost-balanced 1.16-1.21.
         int64_t begin = (n * rank) / world, end = (n * (rank + 1)) / world;
-        if (world > 1 && !(opt.flags & PD_NO_BALANCE) && n >= 4 * world) {
+        if (world > 1 && (opt.flags & PD_BALANCE) && n >= 4 * world) {
             const int64_t stride = std::max<int64_t>(1, n / 40000);
             const int64_t ns = (n + stride - 1) / stride;
             std::vector<int32_t> hpos(ns);
@@ -546,7 +547,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         for (int k = 0; k < 3; ++k) s.tier_cells[k] = (int64_t)hs.tier[k];
         s.overflow_cells = (int64_t)hs.overflow;
         s.queue_spills = (int64_t)hs.spills;
-        for (int k = 0; k < 6; ++k) s.warp_cycles[k] = (int64_t)hs.cyc[k];
+        for (int k = 0; k < 10; ++k) s.warp_cycles[k] = (int64_t)hs.cyc[k];
         s.nnz = nnz;
         s.ms_bvh = t01;
         s.ms_cells = t12;

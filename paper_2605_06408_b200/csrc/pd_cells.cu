@@ -221,7 +221,7 @@ enum { CLIP_NONE = 0, CLIP_DONE = 1, CLIP_EMPTY = 2, CLIP_OVF = 3 };
 
 struct Counters {
     unsigned long long nodes, leaves, sites, tests, clips, spills;
-    unsigned long long cyc[6];  // PD_PROFILE builds: warp cycles in init, descend, leaf, clip, pop, finalize
+    unsigned long long cyc[10];  // PD_PROFILE: init, descend, leaf, clip, pop, finalize | clip: classify, boundary, create, aabb
 };
 #ifndef PD_PROFILE
 #define PD_PROFILE 0
@@ -416,7 +416,8 @@ __device__ __forceinline__ double4 exact_plane(const Cell& c, float4 sj) {
 }
 
 template <class T>
-__device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, FPlane f, int pidn) {
+__device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, FPlane f, int pidn, Counters& cnt) {
+    PT_BEGIN(t_cls);
     // FP64 tolerance for certification (only evaluated on ambiguous classifications)
     const double tol = 1e-12 * (double)sqrtf(f.nx * f.nx + f.ny * f.ny + f.nz * f.nz) * (double)c.rmax;
     // warp-uniform counts snapshotted in registers; published to the shared Cell only at the end,
@@ -445,9 +446,11 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
         if (lane == 0) S.omask[ch] = m;
         R += __popc(m);
     }
+    PT_END(t_cls, 6);
     if (R == 0) return CLIP_NONE;
     if (R == nv0) return CLIP_EMPTY;
     __syncwarp();
+    PT_BEGIN(t_bnd);
     const double4 pl = exact_plane(c, sj);
     int np0 = c.np;
     if (np0 >= (T::PMAX * 85) / 100) {  // plane garbage collection (vertex slots are unaffected)
@@ -548,6 +551,8 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
             __syncwarp();
         }
     }
+    PT_END(t_bnd, 7);
+    PT_BEGIN(t_cre);
     int nvn = nv0 - R + B;
     if (nvn > T::VMAX || B > T::VMAX || np0 + 1 > T::PMAX) return CLIP_OVF;
     // 3. append the plane, create (h, x, y) for every boundary edge
@@ -589,8 +594,11 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
     c.nv = nvn;  // safe without a prior sync: no lane reads c.nv/c.np in clip after the snapshot
     c.np = hs + 1;
     __syncwarp();
+    PT_END(t_cre, 8);
+    PT_BEGIN(t_ab);
     if (PD_FUSED_AABB) finish_aabb(c, box);
     else update_aabb(S, c, lane);
+    PT_END(t_ab, 9);
     return CLIP_DONE;
 }
 
@@ -690,7 +698,7 @@ __device__ PD_INL_LEAF int process_leaf(WarpState<T>& S, Cell& c, int lane, int 
         f.d = 0.5f * (f2 + fdq);
         f.m = 1e-6f * ((fabsf(f.nx) + fabsf(f.ny) + fabsf(f.nz)) * c.vmax + f2 + fabsf(fdq));
         PT_BEGIN(t_clip);
-        int st = clip(S, c, lane, make_float4(sx, sy, sz, sw), f, first + src);
+        int st = clip(S, c, lane, make_float4(sx, sy, sz, sw), f, first + src, cnt);
         PT_END(t_clip, 3);
         if (st == CLIP_EMPTY) return ST_EMPTY;
         if (st == CLIP_OVF) return ST_OVERFLOW;
@@ -745,7 +753,11 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     }
                     culled = !((surv >> lane) & 1u);
                 }
-                if (!surv) { have = false; break; }
+                if (!surv) {
+                    have = false;
+                    PT_END(t_desc, 1);
+                    break;
+                }
                 // go to the child with the smallest priority delta, queue the other survivors
                 int kmin = __reduce_min_sync(FULL, culled ? 0x7fffffff : ford(key));
                 int near = __ffs(__ballot_sync(FULL, !culled && ford(key) == kmin)) - 1;
@@ -1049,7 +1061,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
     WarpState<T>& S = T::GLOBAL ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x * T::WARPS + wid]
                                 : reinterpret_cast<WarpState<T>*>(smem_raw)[wid];
     const int64_t total = P.list ? (int64_t)(*P.list_count) : P.count;
-    Counters cnt = {0, 0, 0, 0, 0, 0, {0, 0, 0, 0, 0, 0}};
+    Counters cnt = {0, 0, 0, 0, 0, 0, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
     const int gw = blockIdx.x * T::WARPS + wid;
     NodeChild* spill = P.spill + (size_t)gw * P.spill_cap;
     for (int k = lane; k < T::EBW; k += 32) S.ebits[k] = 0u;
@@ -1065,7 +1077,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             int64_t idx = b0 + b;
             int s = P.list ? P.list[idx] : (int)(P.begin + idx);
             Cell& c = S.c;
-            const Counters before = cnt;
+            const long long t_cell0 = (P.flags & PD_COST) ? clock64() : 0;
             float4 site = __ldg(&P.sites[s]);
             c.fpx = site.x; c.fpy = site.y; c.fpz = site.z; c.fpw = site.w;
             c.px = site.x; c.py = site.y; c.pz = site.z; c.pw = site.w;
@@ -1088,9 +1100,9 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             finalize(S, c, lane, P, st);
             PT_END(t_fin, 5);
             ncells++;
-            if ((P.flags & PD_COST) && lane == 0) {
-                unsigned long long w = (cnt.nodes - before.nodes) + (cnt.sites - before.sites) + 8 * (cnt.clips - before.clips);
-                P.out.cost[c.self_orig] = (int32_t)min(w, 0x7fffffffull);
+            if ((P.flags & PD_COST) && lane == 0) {  // the cell's warp time, in units of 64 SM cycles
+                const long long w = (clock64() - t_cell0) >> 6;
+                P.out.cost[c.self_orig] = (int32_t)min(max(w, 1ll), 0x7fffffffll);
             }
             __syncwarp();
         }
@@ -1106,7 +1118,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
         red_add_g(&P.stats->overflow, novf);
         red_add_g(&P.stats->spills, cnt.spills);
         if (P.prof_tier < 0 || P.prof_tier == tier)
-            for (int k = 0; k < 6; ++k) red_add_g(&P.stats->cyc[k], cnt.cyc[k]);
+            for (int k = 0; k < 10; ++k) red_add_g(&P.stats->cyc[k], cnt.cyc[k]);
     }
 }
 

@@ -50,7 +50,7 @@ struct CellOut {
 };
 
 struct Stats {  // device counters (PD_STATS)
-    unsigned long long nodes, leaves, sites, clip_tests, clips, cells, tier[3], overflow, spills, cyc[6];
+    unsigned long long nodes, leaves, sites, clip_tests, clips, cells, tier[3], overflow, spills, cyc[10];
 };
 
 struct CellParams {

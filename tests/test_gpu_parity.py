@@ -203,7 +203,7 @@ def test_sharded_reassembly_matches_single():
     ref = _gpu(wl)
     p = torch.from_numpy(wl.points).cuda()
     w = torch.from_numpy(wl.weights).cuda()
-    for world, fl in ((2, 0), (3, 0), (3, pd.NO_BALANCE)):
+    for world, fl in ((2, 0), (3, 0), (3, pd.BALANCE)):
         parts = []
         perm = None
         bounds = []
@@ -213,7 +213,7 @@ def test_sharded_reassembly_matches_single():
             parts.append(pd.export_slice(d))
             if perm is None:
                 perm = pd.morton_perm(d).clone()
-        # slices tile the Morton order (equal-cost cuts by default, equal-count with NO_BALANCE)
+        # slices tile the Morton order (equal-count by default, equal-cost with BALANCE)
         assert bounds[0][0] == 0 and bounds[-1][1] == wl.n
         assert all(bounds[r][1] == bounds[r + 1][0] for r in range(world - 1))
         cat = [torch.cat([pp[k] for pp in parts]) for k in range(6)]

@@ -1,6 +1,6 @@
 """Load balance of the seed-sharded build, measured on ONE GPU by building each rank's slice in turn:
 max/mean of per-slice cell-kernel time = the imbalance a world-N run would see.
-Equal-count slices (PD_NO_BALANCE) vs cost-balanced slices (default)."""
+Equal-count slices (default) vs cost-balanced slices (PD_BALANCE)."""
 import json
 import os
 import sys
@@ -21,7 +21,7 @@ for cfg in cfgs:
         del_ = pd.build_diagram(p, w, wl.box)
         torch.cuda.synchronize()
         del del_
-    for name, fl in (("equal_count", pd.NO_BALANCE), ("cost_balanced", 0)):
+    for name, fl in (("equal_count", 0), ("cost_balanced", pd.BALANCE)):
         per, tot = [], []
         for r in range(world):
             d = pd.build_diagram(p, w, wl.box, shard_rank=r, shard_world=world, flags=fl | pd.STATS)
