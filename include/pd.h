@@ -59,7 +59,7 @@ enum {
     PD_ISOTROPIC = 1u << 3,   /* ablation: isotropic radius instead of the directional one */
     PD_DFS = 1u << 4,         /* ablation: depth-first LIFO traversal instead of best-first */
     PD_PAPER_BOUND = 1u << 6, /* ablation: the paper's culling bounds only (no AABB-support companion) */
-    PD_COST = 1u << 7,        /* record per-cell work (pd_cell_cost): the cell's warp time in 64-cycle units */
+    PD_COST = 1u << 7,        /* record per-cell work (pd_cell_cost): BVH nodes + leaf sites + 8 x clips (deterministic) */
     PD_EXACT_NODES = 1u << 8, /* exact polytope-vs-box node test on every node the AABB tests keep */
     PD_NO_EXACT = 1u << 9,    /* never use the exact polytope-vs-box node test (pure AABB culling) */
     PD_BALANCE = 1u << 10     /* sharded build: equal-cost Morton slices from a sampled cost estimate
@@ -125,7 +125,7 @@ const float* pd_face_areas(const pd_result* r);  /* nnz; aligned with pd_neighbo
 const float* pd_volumes(const pd_result* r);     /* n; 0 for EMPTY */
 const float* pd_surface(const pd_result* r);     /* n; total surface area incl. box walls */
 const uint8_t* pd_cell_flags(const pd_result* r);/* n; PD_CELL_* bits */
-const int32_t* pd_cell_cost(const pd_result* r); /* n (device); per-cell warp time (64-cycle units), only with PD_COST, else NULL */
+const int32_t* pd_cell_cost(const pd_result* r); /* n (device); per-cell work count, only with PD_COST, else NULL */
 pd_status pd_get_stats(const pd_result* r, pd_stats* s);
 void pd_free(pd_result* r);
 

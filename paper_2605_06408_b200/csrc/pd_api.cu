@@ -347,9 +347,9 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             return ev ? atoi(ev) : 200;
         }();
         // ---- slice of the Morton order owned by this rank: equal-count by default;
-        // PD_BALANCE cuts equal estimated cost, from the tier-1 kernel's per-cell warp time on a strided
-        // ~40k-cell sample (deterministic, so every rank computes the same cuts).  Measured on C4 at
-        // world 8 (tools/shard_balance.py): equal-count max/mean 1.07, cost-balanced 1.16-1.21.
+        // PD_BALANCE cuts equal estimated cost, from the tier-1 kernel's per-cell work counters on a
+        // strided ~40k-cell sample (deterministic, so every rank computes the same cuts).  Measured on
+        // C4 at world 8 (tools/shard_balance.py): equal-count max/mean 1.07, cost-balanced 1.16.
         int64_t begin = (n * rank) / world, end = (n * (rank + 1)) / world;
         if (world > 1 && (opt.flags & PD_BALANCE) && n >= 4 * world) {
             const int64_t stride = std::max<int64_t>(1, n / 40000);

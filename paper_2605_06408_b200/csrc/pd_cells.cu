@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             int64_t idx = b0 + b;
             int s = P.list ? P.list[idx] : (int)(P.begin + idx);
             Cell& c = S.c;
-            const long long t_cell0 = (P.flags & PD_COST) ? clock64() : 0;
+            const Counters before = cnt;
             float4 site = __ldg(&P.sites[s]);
             c.fpx = site.x; c.fpy = site.y; c.fpz = site.z; c.fpw = site.w;
             c.px = site.x; c.py = site.y; c.pz = site.z; c.pw = site.w;
@@ -1100,9 +1100,9 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             finalize(S, c, lane, P, st);
             PT_END(t_fin, 5);
             ncells++;
-            if ((P.flags & PD_COST) && lane == 0) {  // the cell's warp time, in units of 64 SM cycles
-                const long long w = (clock64() - t_cell0) >> 6;
-                P.out.cost[c.self_orig] = (int32_t)min(max(w, 1ll), 0x7fffffffll);
+            if ((P.flags & PD_COST) && lane == 0) {  // deterministic work count (balanced cuts must agree)
+                unsigned long long w = (cnt.nodes - before.nodes) + (cnt.sites - before.sites) + 8 * (cnt.clips - before.clips);
+                P.out.cost[c.self_orig] = (int32_t)min(w, 0x7fffffffull);
             }
             __syncwarp();
         }
