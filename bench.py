@@ -181,7 +181,10 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
+    base_flags = pd.WARM_START if args.warm_start else 0
+
     def step(flags=0):
+        flags |= base_flags
         if world > 1:
             return pddist.build_diagram_distributed(p, w, wl.box, leaf_size=args.leaf, flags=flags)
         return pd.build_diagram(p, w, wl.box, leaf_size=args.leaf, flags=flags)
@@ -191,7 +194,8 @@ def run_ours(args):
         del d
     torch.cuda.synchronize()
     # stats pass (counters), not timed
-    d = pd.build_diagram(p, w, wl.box, leaf_size=args.leaf, flags=pd.STATS, shard_rank=rank, shard_world=world)
+    d = pd.build_diagram(p, w, wl.box, leaf_size=args.leaf, flags=pd.STATS | base_flags, shard_rank=rank,
+                         shard_world=world)
     stats = dict(d.stats)
     nnz_total = int(d.nnz)
     flags_np = d.flags.cpu().numpy()
@@ -235,7 +239,7 @@ def run_ours(args):
         t0 = time.perf_counter()
         pts = hp.numpy()
         d = pd.build_diagram(pts, None if hw is None else hw.numpy(), wl.box, leaf_size=args.leaf, out_host=True,
-                             shard_rank=rank, shard_world=world)
+                             flags=base_flags, shard_rank=rank, shard_world=world)
         dt = time.perf_counter() - t0
         d2h = (d.n + 1) * 8 + d.nnz * 8 + d.n * 9
         del d
@@ -265,6 +269,7 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
                 "config": {"workload": f"{wl.name}: {wl.description}", "n": wl.n, "box": list(wl.box),
                            "leaf_size": args.leaf or 32, "parallelism": f"seed-sharded x{world}",
+                           "warm_start": bool(args.warm_start),
                            "l2": "flushed before every timed step (256 MiB write)", "generation_s": round(gen_s, 1)},
                 "roofline": roof,
                 "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
@@ -294,6 +299,7 @@ def main():
     ap.add_argument("--leaf", type=int, default=0)
     ap.add_argument("--ref-cells", type=int, default=64, help="reference arm: cells per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--warm-start", action="store_true", help="KNN warm start (PAPER.md:544-545)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

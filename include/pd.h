@@ -58,6 +58,9 @@ enum {
     PD_STATS = 1u << 2,       /* collect traversal/clipping counters (pd_get_stats) */
     PD_ISOTROPIC = 1u << 3,   /* ablation: isotropic radius instead of the directional one */
     PD_DFS = 1u << 4,         /* ablation: depth-first LIFO traversal instead of best-first */
+    PD_WARM_START = 1u << 5,  /* KNN warm start (K = 8): a K-nearest-neighbour query on the
+                                 same BVH pre-clips every cell before its traversal; same diagram, different
+                                 work (the neighbour sets are identical, areas/volumes agree to rounding) */
     PD_PAPER_BOUND = 1u << 6, /* ablation: the paper's culling bounds only (no AABB-support companion) */
     PD_COST = 1u << 7,        /* record per-cell work (pd_cell_cost): BVH nodes + leaf sites + 8 x clips (deterministic) */
     PD_EXACT_NODES = 1u << 8, /* exact polytope-vs-box node test on every node the AABB tests keep */
@@ -99,6 +102,7 @@ typedef struct {
     double ms_tier[3];         /* cell-kernel time per capacity tier (CUDA events) */
     int64_t warp_cycles[10];   /* PD_PROFILE builds only: warp clock64 in init/descend/leaf/clip/pop/finalize,
                                   then clip's classify/boundary/create/aabb */
+    double ms_knn;             /* PD_WARM_START: the K-nearest-neighbour query (part of ms_cells) */
 } pd_stats;
 
 typedef struct pd_result pd_result;

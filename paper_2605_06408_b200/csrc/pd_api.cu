@@ -388,6 +388,8 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             Q.gstate = gstate;
             Q.exact_after = exact_after;
             Q.prof_tier = -2;
+            Q.coop_min_v = 128;
+            Q.trace_cell = -1;
             Q.work_counter = sctr;
             Q.last_tier = 1;  // heavy sampled cells keep their (partial) cost instead of escalating
             Q.list = spos;
@@ -414,6 +416,17 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         }
         r->slice_begin = begin;
         r->slice_end = end;
+        // ---- optional KNN warm start: K = 8 nearest sites of every site of the slice
+        int32_t* knn = nullptr;
+        cudaEvent_t kev[2] = {nullptr, nullptr};
+        if (opt.flags & PD_WARM_START) {
+            knn = W.alloc<int32_t>((size_t)n * pd::KNN_K);
+            ck(cudaEventCreate(&kev[0]));
+            ck(cudaEventCreate(&kev[1]));
+            ck(cudaEventRecord(kev[0], st));
+            ck(pd::knn_query(sorted, bvh.nodes, bvh.root, (int)begin, (int)end, knn, sms, st, &launches));
+            ck(cudaEventRecord(kev[1], st));
+        }
         int32_t* lists = W.alloc<int32_t>(2 * (size_t)std::max<int64_t>(end - begin, 1));
         unsigned long long* counters = W.alloc<unsigned long long>(8);
         int32_t* list_counts = W.alloc<int32_t>(4);
@@ -467,6 +480,10 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.gstate = gstate;
             P.exact_after = exact_after;
             P.prof_tier = getenv("PD_PROF_TIER") ? atoi(getenv("PD_PROF_TIER")) : -1;
+            P.knn = knn;
+            P.start_tier = getenv("PD_START_TIER") ? atoi(getenv("PD_START_TIER")) : 0;
+            P.coop_min_v = getenv("PD_COOP_MIN_V") ? atoi(getenv("PD_COOP_MIN_V")) : 128;
+            P.trace_cell = getenv("PD_TRACE_CELL") ? atoi(getenv("PD_TRACE_CELL")) : -1;
             int64_t L = end - begin;
             for (int tier = 0; tier < 3; ++tier) {
                 P.work_counter = counters + tier;
@@ -538,6 +555,14 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             s.ms_tier[k] = tt;
         }
         for (auto& e : tev) cudaEventDestroy(e);
+        s.ms_knn = 0.0;
+        if (kev[0]) {
+            float tk = 0.f;
+            cudaEventElapsedTime(&tk, kev[0], kev[1]);
+            s.ms_knn = tk;
+            cudaEventDestroy(kev[0]);
+            cudaEventDestroy(kev[1]);
+        }
         s.cells = (int64_t)hs.cells;
         s.nodes_visited = (int64_t)hs.nodes;
         s.leaves_visited = (int64_t)hs.leaves;

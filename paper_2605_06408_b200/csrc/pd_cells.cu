@@ -26,6 +26,7 @@
 //   * capacity tiers: cells that outgrow the tier's on-chip arrays are handed to a larger tier.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include <type_traits>
 
@@ -64,9 +65,11 @@ constexpr unsigned FULL = 0xffffffffu;
 #define PD_EDGE_BITMAP 0
 #endif
 
-template <int V, int P, int Q, int W, int MINB, bool GLOB = false>
+template <int V, int P, int Q, int W, int MINB, bool GLOB = false, bool CO = false>
 struct TierCfg {
     static constexpr bool GLOBAL = GLOB;     // warp state in global memory (top tier) instead of smem
+    // CTA-cooperative cell (top tier): warp 0 runs the cell program, warps 1..W-1 join its O(V) passes
+    static constexpr bool COOP = CO;
     using trip_t = typename std::conditional<(P <= 1024), uint32_t, uint64_t>::type;
     static constexpr int VMAX = V;   // vertices
     static constexpr int PMAX = P;   // planes (<= 1024: 10-bit triplet fields)
@@ -96,7 +99,15 @@ using Tier1 = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, 4, PD_T1_MINB>;
 using Tier2 = TierCfg<384, 192, 256, 4, 1>;
 // Top tier: state in global memory (L1/L2-cached), 64-bit plane-index triplets; for the rare cells
 // with thousands of faces (heavy-tailed weights, SURVEY.md §7 hard part 3).
-using Tier3 = TierCfg<16384, 8192, 4096, 2, 1, true>;
+// One cell per CTA: its 16 warps share every O(V) pass (classification, exact node tests, AABB,
+// finalize) of the heavy cells (heavy-tailed weights: thousands of vertices).
+#ifndef PD_T3_COOP
+#define PD_T3_COOP 1
+#endif
+#ifndef PD_T3_WARPS
+#define PD_T3_WARPS 16
+#endif
+using Tier3 = TierCfg<16384, 8192, 4096, PD_T3_COOP ? PD_T3_WARPS : 2, 1, true, PD_T3_COOP != 0>;
 constexpr int kTier3BlocksPerSM = 1;
 
 // Per-warp cell state (warp-uniform).  Lives in the warp's shared-memory block (read by broadcast):
@@ -202,7 +213,7 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // Compile-time culling/traversal mode.  Tier 1 is instantiated per common mode so that the default
 // kernel carries none of the ablation branches (instruction-fetch stalls dominate otherwise);
 // kDynMode reads the mode bits from the runtime flags (mode combinations, tiers 2-3).
-constexpr unsigned kModeBits = PD_ISOTROPIC | PD_DFS | PD_PAPER_BOUND | PD_EXACT_NODES | PD_NO_EXACT;
+constexpr unsigned kModeBits = PD_ISOTROPIC | PD_DFS | PD_PAPER_BOUND | PD_EXACT_NODES | PD_NO_EXACT | PD_WARM_START;
 constexpr unsigned kDynMode = 0xffffffffu;
 template <unsigned MODE>
 __device__ __forceinline__ unsigned mode_flags(unsigned runtime_flags) {
@@ -292,26 +303,84 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
     return d2 + dwn - r2;
 }
 
+// ---------------------------------------------------------------- CTA-cooperative passes (top tier)
+// Warp 0 of a COOP CTA runs the cell program; at an O(V) pass it publishes a job in shared memory and
+// meets warps 1..W-1 at named barrier 1, every warp takes a strided share of the vertex (or face)
+// slots, and all meet again at barrier 2, after which warp 0 combines the per-warp partials in a fixed
+// order (so the result is deterministic).
+enum { JOB_EXIT = 0, JOB_CLASSIFY = 1, JOB_EXACT = 2, JOB_AABB = 3, JOB_TWINS = 4, JOB_AREAS = 5 };
+constexpr int kCoopMaxW = 32;
+struct CoopJob {
+    int kind, nv, np;
+    int min_v;  // passes over fewer vertices stay on warp 0 (CellParams::coop_min_v)
+    unsigned mask;
+    FPlane f;
+    float4 sj;
+    double tol;
+    float4 lo[WIDE], hi[WIDE];
+    int ipart[kCoopMaxW][WIDE];
+    double dpart[kCoopMaxW][2];
+};
+extern __shared__ __align__(16) unsigned char pd_smem[];
+__device__ __forceinline__ CoopJob& coop_job() { return *reinterpret_cast<CoopJob*>(pd_smem); }
+template <class T>
+__device__ __forceinline__ int P_coop_min_v(const WarpState<T>&) { return coop_job().min_v; }
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // Exact polytope-vs-box node test (not in the paper; strictly tighter than any AABB bound).  The
 // plane of p_j (D = p_j - p_i) cuts the cell iff some vertex v has v.D - |D|^2/2 > (w_i - w_j)/2.
 // Over all p_j in the box, D_k in [a_k, b_k] and w_j <= w_max, and
 //   max_{D in box} (v.D - |D|^2/2) = sum_k (v_k c_k - c_k^2/2),  c_k = clamp(v_k, a_k, b_k),
 // (a separable concave maximisation), so the node is culled iff for every vertex that sum is
 // <= (w_i - w_max)/2.  Lanes = vertices, FP32 with a 1e-5 relative margin (only keeps nodes).
-template <class T>
-__device__ __noinline__ bool node_exact_culled(const WarpState<T>& S, const Cell& c, int lane, float4 lo_w, float4 hi_l) {
+__device__ __forceinline__ float exact_partial(const float4* fv, const Cell& c, float4 lo_w, float4 hi_l, int s0, int nv,
+                                               int stride) {
     const float a0 = lo_w.x - c.fpx, a1 = lo_w.y - c.fpy, a2 = lo_w.z - c.fpz;
     const float b0 = hi_l.x - c.fpx, b1 = hi_l.y - c.fpy, b2 = hi_l.z - c.fpz;
     float best = -INFINITY;
-    for (int s = lane; s < c.nv; s += 32) {
-        float4 v = S.fv[s];
+    for (int s = s0; s < nv; s += stride) {
+        float4 v = fv[s];
         float cx = fminf(fmaxf(v.x, a0), b0), cy = fminf(fmaxf(v.y, a1), b1), cz = fminf(fmaxf(v.z, a2), b2);
         best = fmaxf(best, cx * (v.x - 0.5f * cx) + cy * (v.y - 0.5f * cy) + cz * (v.z - 0.5f * cz));
     }
-    best = iford(__reduce_max_sync(FULL, ford(best)));
+    return best;
+}
+__device__ __forceinline__ bool exact_decide(const Cell& c, float4 lo_w, float4 hi_l, float best) {
+    const float a0 = lo_w.x - c.fpx, a1 = lo_w.y - c.fpy, a2 = lo_w.z - c.fpz;
+    const float b0 = hi_l.x - c.fpx, b1 = hi_l.y - c.fpy, b2 = hi_l.z - c.fpz;
     const float B0 = fmaxf(fabsf(a0), fabsf(b0)), B1 = fmaxf(fabsf(a1), fabsf(b1)), B2 = fmaxf(fabsf(a2), fabsf(b2));
     const float mag = B0 * (c.vmax + B0) + B1 * (c.vmax + B1) + B2 * (c.vmax + B2) + fabsf(c.fpw) + fabsf(lo_w.w);
     return best < 0.5f * (c.fpw - lo_w.w) - 1e-5f * mag;
+}
+
+template <class T>
+__device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int lane);
+
+// warp 0: run the published job with all warps of the CTA
+template <class T>
+__device__ __forceinline__ void coop_go(WarpState<T>& S, CoopJob& J, int lane) {
+    __syncwarp();
+    named_bar(1, T::WARPS * 32);
+    coop_run<T>(S, J, 0, lane);
+    named_bar(2, T::WARPS * 32);
+}
+
+template <class T>
+__device__ __noinline__ bool node_exact_culled(const WarpState<T>& S, const Cell& c, int lane, float4 lo_w, float4 hi_l) {
+    float best;
+    if (T::COOP && c.nv >= P_coop_min_v(S)) {
+        CoopJob& J = coop_job();
+        if (lane == 0) { J.kind = JOB_EXACT; J.nv = c.nv; J.mask = 1u; J.lo[0] = lo_w; J.hi[0] = hi_l; }
+        coop_go<T>(const_cast<WarpState<T>&>(S), J, lane);
+        int b = lane < T::WARPS ? J.ipart[lane][0] : ford(-INFINITY);
+        best = iford(__reduce_max_sync(FULL, b));
+    } else {
+        best = exact_partial(S.fv, c, lo_w, hi_l, lane, c.nv, 32);
+        best = iford(__reduce_max_sync(FULL, ford(best)));
+    }
+    return exact_decide(c, lo_w, hi_l, best);
 }
 
 // Per-lane partial AABB of vertex positions (FP32 copies).
@@ -354,7 +423,17 @@ template <class T>
 __device__ PD_INL_AABB void update_aabb(const WarpState<T>& S, Cell& c, int lane) {
     Box6 b;
     b.reset();
-    for (int s = lane; s < c.nv; s += 32) b.add(S.fv[s]);
+    if (T::COOP && c.nv >= P_coop_min_v(S)) {
+        CoopJob& J = coop_job();
+        if (lane == 0) { J.kind = JOB_AABB; J.nv = c.nv; }
+        coop_go<T>(const_cast<WarpState<T>&>(S), J, lane);
+        if (lane < T::WARPS) {
+            b.lo0 = iford(J.ipart[lane][0]); b.lo1 = iford(J.ipart[lane][1]); b.lo2 = iford(J.ipart[lane][2]);
+            b.hi0 = iford(J.ipart[lane][3]); b.hi1 = iford(J.ipart[lane][4]); b.hi2 = iford(J.ipart[lane][5]);
+        }
+    } else {
+        for (int s = lane; s < c.nv; s += 32) b.add(S.fv[s]);
+    }
     finish_aabb(c, b);
 }
 
@@ -415,6 +494,32 @@ __device__ __forceinline__ double4 exact_plane(const Cell& c, float4 sj) {
     return make_double4(ex, ey, ez, 0.5 * (ex * ex + ey * ey + ez * ez + (c.pw - (double)sj.w)));
 }
 
+// Removed-vertex slots (ascending) from the per-chunk outside ballots; returns their number.
+template <class T>
+__device__ __noinline__ int rem_from_omask(WarpState<T>& S, int nch, int lane) {
+    int R = 0;
+    for (int c0 = 0; c0 < nch; c0 += 32) {
+        const int ch = c0 + lane;
+        unsigned m = ch < nch ? S.omask[ch] : 0u;
+        const int k = __popc(m);
+        int inc = k;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int v = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += v;
+        }
+        int off = R + inc - k;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            S.rem[off++] = (uint16_t)(ch * 32 + b);
+        }
+        R += __shfl_sync(FULL, inc, 31);
+    }
+    __syncwarp();
+    return R;
+}
+
 template <class T>
 __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, FPlane f, int pidn, Counters& cnt) {
     PT_BEGIN(t_cls);
@@ -428,6 +533,12 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
     const int nch = (nv0 + 31) >> 5;
     Box6 box;  // AABB of the kept vertices, fused into the classification pass
     box.reset();
+    if (T::COOP && nv0 >= P_coop_min_v(S)) {  // all warps of the CTA classify; removed slots from the ballots
+        CoopJob& J = coop_job();
+        if (lane == 0) { J.kind = JOB_CLASSIFY; J.nv = nv0; J.f = f; J.sj = sj; J.tol = tol; }
+        coop_go<T>(S, J, lane);
+        R = rem_from_omask(S, nch, lane);
+    } else
     for (int ch = 0; ch < nch; ++ch) {
         int s = ch * 32 + lane;
         bool out = false;
@@ -637,12 +748,12 @@ __device__ __noinline__ bool cuts_fp64(const WarpState<T>& S, const Cell& c, flo
     return false;
 }
 
+// Candidate processing (lane = candidate site j, Morton index): a BVH leaf's sites, or the warm
+// start's K nearest sites.
 template <class T, unsigned MODE>
-__device__ PD_INL_LEAF int process_leaf(WarpState<T>& S, Cell& c, int lane, int link, const CellParams& P, Counters& cnt) {
+__device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int j, bool valid, int count,
+                                         const CellParams& P, Counters& cnt) {
     const unsigned flags = mode_flags<MODE>(P.flags);
-    const int first = leaf_first(link), count = leaf_count(link);
-    const int j = first + lane;
-    bool valid = lane < count && j != c.self;
     float4 sj = make_float4(0.f, 0.f, 0.f, 0.f);
     float Dx = 0.f, Dy = 0.f, Dz = 0.f, D2 = 0.f, dq = 0.f;
     bool dup_kill = false;
@@ -698,7 +809,8 @@ __device__ PD_INL_LEAF int process_leaf(WarpState<T>& S, Cell& c, int lane, int 
         f.d = 0.5f * (f2 + fdq);
         f.m = 1e-6f * ((fabsf(f.nx) + fabsf(f.ny) + fabsf(f.nz)) * c.vmax + f2 + fabsf(fdq));
         PT_BEGIN(t_clip);
-        int st = clip(S, c, lane, make_float4(sx, sy, sz, sw), f, first + src, cnt);
+        const int jsrc = __shfl_sync(FULL, j, src);
+        int st = clip(S, c, lane, make_float4(sx, sy, sz, sw), f, jsrc, cnt);
         PT_END(t_clip, 3);
         if (st == CLIP_EMPTY) return ST_EMPTY;
         if (st == CLIP_OVF) return ST_OVERFLOW;
@@ -709,6 +821,22 @@ __device__ PD_INL_LEAF int process_leaf(WarpState<T>& S, Cell& c, int lane, int 
         mask = __ballot_sync(FULL, cand);
     }
     return ST_OK;
+}
+
+template <class T, unsigned MODE>
+__device__ __forceinline__ int process_leaf(WarpState<T>& S, Cell& c, int lane, int link, const CellParams& P, Counters& cnt) {
+    const int first = leaf_first(link), count = leaf_count(link);
+    const int j = first + lane;
+    return process_cands<T, MODE>(S, c, lane, j, lane < count && j != c.self, count, P, cnt);
+}
+
+// KNN warm start: clip by the site's K nearest sites before the traversal.  Those
+// sites are met again in their leaves, where their planes no longer cut (on-plane vertices are kept,
+// SURVEY.md §8(c) Q11), so the diagram is unchanged; coincident sites are never in the list.
+template <class T, unsigned MODE>
+__device__ __noinline__ int warm_start(WarpState<T>& S, Cell& c, int lane, const CellParams& P, Counters& cnt) {
+    const int j = lane < KNN_K ? __ldg(&P.knn[(int64_t)c.self * KNN_K + lane]) : -1;
+    return process_cands<T, MODE>(S, c, lane, j, j >= 0, KNN_K, P, cnt);
 }
 
 // Best-first traversal (Alg. 1).  Queue entries are the pushed child records;
@@ -744,7 +872,21 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 // internal children too once the cell is heavy
                 const unsigned leafm = __ballot_sync(FULL, lane < WIDE && __float_as_int(hi_l.w) < 0);
                 const unsigned exm = ex_all ? surv : (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) ? (surv & leafm) : 0u);
-                if (exm) {
+                if (exm && T::COOP && c.nv >= P_coop_min_v(S)) {  // all children in one CTA-wide pass
+                    CoopJob& J = coop_job();
+                    const bool mine = lane < WIDE && ((exm >> lane) & 1u);
+                    if (mine) { J.lo[lane] = lo_w; J.hi[lane] = hi_l; }
+                    if (lane == 0) { J.kind = JOB_EXACT; J.nv = c.nv; J.mask = exm; }
+                    coop_go<T>(S, J, lane);
+                    bool cull = false;
+                    if (mine) {
+                        int b = J.ipart[0][lane];
+                        for (int w = 1; w < T::WARPS; ++w) b = max(b, J.ipart[w][lane]);
+                        cull = exact_decide(c, lo_w, hi_l, iford(b));
+                    }
+                    surv &= ~__ballot_sync(FULL, cull);
+                    culled = !((surv >> lane) & 1u);
+                } else if (exm) {
                     unsigned s2 = exm;
                     while (s2) {
                         int k = __ffs(s2) - 1;
@@ -940,6 +1082,122 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
     update_aabb(S, c, lane);
 }
 
+// Twins: the vertex across each directed edge of vertex u (slots u0, u0+stride, ...).
+template <class T>
+__device__ __forceinline__ void twins_range(WarpState<T>& S, int nv, int u0, int stride) {
+    for (int u = u0; u < nv; u += stride) {
+        auto t = S.vt[u];
+        int a = ta(t), b = tb(t), cc = tc(t);
+        uint16_t t0 = 0xffff, t1 = 0xffff, t2 = 0xffff;
+#pragma unroll 1
+        for (int k = 0; k < nv; ++k) {
+            auto w = S.vt[k];
+            if (has_edge(w, b, a)) t0 = (uint16_t)k;
+            if (has_edge(w, cc, b)) t1 = (uint16_t)k;
+            if (has_edge(w, a, cc)) t2 = (uint16_t)k;
+        }
+        S.tw[0][u] = t0; S.tw[1][u] = t1; S.tw[2][u] = t2;
+    }
+}
+
+// Face vector areas (1/2 sum v x next(v)), face areas, and this thread's volume / surface partials
+// (faces f0, f0+stride, ...).
+template <class T>
+__device__ __forceinline__ void areas_range(WarpState<T>& S, int nv, int np, int f0, int stride, double& vol, double& surf) {
+    for (int f = f0; f < np; f += stride) {
+        double Ax = 0, Ay = 0, Az = 0;
+#pragma unroll 1
+        for (int u = 0; u < nv; ++u) {
+            auto t = S.vt[u];
+            int which = ta(t) == f ? 2 : (tb(t) == f ? 0 : (tc(t) == f ? 1 : -1));
+            if (which >= 0) {
+                int w = S.tw[which][u];
+                if (w == 0xffff) continue;
+                double ux = S.vx[u], uy = S.vy[u], uz = S.vz[u];
+                double wx = S.vx[w], wy = S.vy[w], wz = S.vz[w];
+                Ax += uy * wz - uz * wy;
+                Ay += uz * wx - ux * wz;
+                Az += ux * wy - uy * wx;
+            }
+        }
+        Ax *= 0.5; Ay *= 0.5; Az *= 0.5;
+        double area = sqrt(Ax * Ax + Ay * Ay + Az * Az);
+        S.farea[f] = area;
+        double4 pl = S.pl[f];
+        double nn = pl.x * pl.x + pl.y * pl.y + pl.z * pl.z;
+        vol += (Ax * pl.x + Ay * pl.y + Az * pl.z) * pl.w / nn;
+        surf += area;
+    }
+}
+
+// One warp's share of a cooperative job (warp w of T::WARPS; warp 0 is the cell's own warp).
+template <class T>
+__device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int lane) {
+    const Cell& c = S.c;
+    const int kind = J.kind, nv = J.nv;
+    constexpr int stride = T::WARPS * 32;
+    if (kind == JOB_CLASSIFY) {  // same certified predicate as clip()
+        const FPlane f = J.f;
+        const float4 sj = J.sj;
+        const double tol = J.tol;
+        const int nch = (nv + 31) >> 5;
+        for (int ch = w; ch < nch; ch += T::WARPS) {
+            const int s = ch * 32 + lane;
+            bool out = false;
+            if (s < nv) {
+                float4 v = S.fv[s];
+                float s32 = fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d;
+                if (fabsf(s32) > f.m) out = s32 > 0.f;
+                else {
+                    const double4 pe = exact_plane(c, sj);
+                    out = fma(pe.x, S.vx[s], fma(pe.y, S.vy[s], pe.z * S.vz[s])) - pe.w > tol;
+                }
+            }
+            const unsigned m = __ballot_sync(FULL, out);
+            if (lane == 0) S.omask[ch] = m;
+        }
+    } else if (kind == JOB_EXACT) {
+        const unsigned mask = J.mask;
+        for (int k = 0; k < WIDE; ++k) {
+            if (!((mask >> k) & 1u)) continue;
+            float b = exact_partial(S.fv, c, J.lo[k], J.hi[k], w * 32 + lane, nv, stride);
+            int bi = __reduce_max_sync(FULL, ford(b));
+            if (lane == 0) J.ipart[w][k] = bi;
+        }
+    } else if (kind == JOB_AABB) {
+        Box6 b;
+        b.reset();
+        for (int s = w * 32 + lane; s < nv; s += stride) b.add(S.fv[s]);
+        int r0 = __reduce_min_sync(FULL, ford(b.lo0)), r1 = __reduce_min_sync(FULL, ford(b.lo1)),
+            r2 = __reduce_min_sync(FULL, ford(b.lo2)), r3 = __reduce_max_sync(FULL, ford(b.hi0)),
+            r4 = __reduce_max_sync(FULL, ford(b.hi1)), r5 = __reduce_max_sync(FULL, ford(b.hi2));
+        if (lane == 0) {
+            J.ipart[w][0] = r0; J.ipart[w][1] = r1; J.ipart[w][2] = r2;
+            J.ipart[w][3] = r3; J.ipart[w][4] = r4; J.ipart[w][5] = r5;
+        }
+    } else if (kind == JOB_TWINS) {
+        twins_range(S, nv, w * 32 + lane, stride);
+    } else if (kind == JOB_AREAS) {
+        double vol = 0, surf = 0;
+        areas_range(S, nv, J.np, w * 32 + lane, stride, vol, surf);
+        vol = warp_sum_d(vol);
+        surf = warp_sum_d(surf);
+        if (lane == 0) { J.dpart[w][0] = vol; J.dpart[w][1] = surf; }
+    }
+}
+
+// Warps 1..W-1 of a COOP CTA: serve jobs until warp 0 publishes JOB_EXIT.
+template <class T>
+__device__ __noinline__ void coop_worker(WarpState<T>& S, int w, int lane) {
+    CoopJob& J = coop_job();
+    for (;;) {
+        named_bar(1, T::WARPS * 32);
+        if (*(volatile int*)&J.kind == JOB_EXIT) return;
+        coop_run<T>(S, J, w, lane);
+        named_bar(2, T::WARPS * 32);
+    }
+}
+
 // Face areas (vector area 1/2 sum v x next(v) around each face), volume, neighbours; FP64.
 template <class T>
 __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const CellParams& P, int status) {
@@ -956,51 +1214,22 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
         }
         return;
     }
-    // twins: vertex across each directed edge
-    for (int u = lane; u < c.nv; u += 32) {
-        auto t = S.vt[u];
-        int a = ta(t), b = tb(t), cc = tc(t);
-        uint16_t t0 = 0xffff, t1 = 0xffff, t2 = 0xffff;
-#pragma unroll 1
-        for (int k = 0; k < c.nv; ++k) {
-            auto w = S.vt[k];
-            if (has_edge(w, b, a)) t0 = (uint16_t)k;
-            if (has_edge(w, cc, b)) t1 = (uint16_t)k;
-            if (has_edge(w, a, cc)) t2 = (uint16_t)k;
-        }
-        S.tw[0][u] = t0; S.tw[1][u] = t1; S.tw[2][u] = t2;
-    }
-    __syncwarp();
     double vol = 0, surf = 0;
-    for (int f0 = 0; f0 < c.np; f0 += 32) {
-        int f = f0 + lane;
-        double Ax = 0, Ay = 0, Az = 0;
-        if (f < c.np) {
-#pragma unroll 1
-            for (int u = 0; u < c.nv; ++u) {
-                auto t = S.vt[u];
-                int which = ta(t) == f ? 2 : (tb(t) == f ? 0 : (tc(t) == f ? 1 : -1));
-                if (which >= 0) {
-                    int w = S.tw[which][u];
-                    if (w == 0xffff) continue;
-                    double ux = S.vx[u], uy = S.vy[u], uz = S.vz[u];
-                    double wx = S.vx[w], wy = S.vy[w], wz = S.vz[w];
-                    Ax += uy * wz - uz * wy;
-                    Ay += uz * wx - ux * wz;
-                    Az += ux * wy - uy * wx;
-                }
-            }
-            Ax *= 0.5; Ay *= 0.5; Az *= 0.5;
-            double area = sqrt(Ax * Ax + Ay * Ay + Az * Az);
-            S.farea[f] = area;
-            double4 pl = S.pl[f];
-            double nn = pl.x * pl.x + pl.y * pl.y + pl.z * pl.z;
-            vol += (Ax * pl.x + Ay * pl.y + Az * pl.z) * pl.w / nn;
-            surf += area;
-        }
+    if (T::COOP && c.nv >= P_coop_min_v(S)) {  // twins and faces over all warps of the CTA
+        CoopJob& J = coop_job();
+        if (lane == 0) { J.kind = JOB_TWINS; J.nv = c.nv; J.np = c.np; }
+        coop_go<T>(S, J, lane);
+        if (lane == 0) J.kind = JOB_AREAS;
+        coop_go<T>(S, J, lane);
+        for (int w = 0; w < T::WARPS; ++w) { vol += J.dpart[w][0]; surf += J.dpart[w][1]; }
+        vol /= 3.0;
+    } else {
+        twins_range(S, c.nv, lane, 32);
+        __syncwarp();
+        areas_range(S, c.nv, c.np, lane, 32, vol, surf);
+        vol = warp_sum_d(vol) / 3.0;
+        surf = warp_sum_d(surf);
     }
-    vol = warp_sum_d(vol) / 3.0;
-    surf = warp_sum_d(surf);
     __syncwarp();
     // A face counts when its area exceeds 1e-13 S: below that it is a rounding artefact of a
     // zero-area (edge / vertex) contact of a degenerate configuration (reading R2).
@@ -1054,12 +1283,33 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
     }
 }
 
+__device__ __noinline__ void trace_print(int tier, const Cell& c, const Counters& a, const Counters& b, int st, long long cyc) {
+    printf("PD_TRACE cell=%d tier=%d status=%d nv=%d np=%d cycles=%lld nodes=%llu leaves=%llu sites=%llu tests=%llu "
+           "clips=%llu spills=%llu\n",
+           c.self_orig, tier, st, c.nv, c.np, cyc, a.nodes - b.nodes, a.leaves - b.leaves, a.sites - b.sites,
+           a.tests - b.tests, a.clips - b.clips, a.spills - b.spills);
+    if (PD_PROFILE)
+        printf("PD_TRACE cell=%d phase_cycles init=%llu descend=%llu leaf=%llu clip=%llu pop=%llu finalize=%llu "
+               "classify=%llu boundary=%llu create=%llu aabb=%llu\n",
+               c.self_orig, a.cyc[0] - b.cyc[0], a.cyc[1] - b.cyc[1], a.cyc[2] - b.cyc[2], a.cyc[3] - b.cyc[3],
+               a.cyc[4] - b.cyc[4], a.cyc[5] - b.cyc[5], a.cyc[6] - b.cyc[6], a.cyc[7] - b.cyc[7], a.cyc[8] - b.cyc[8],
+               a.cyc[9] - b.cyc[9]);
+}
+
 template <class T, unsigned MODE>
 __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(CellParams P, int tier) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    WarpState<T>& S = T::GLOBAL ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x * T::WARPS + wid]
-                                : reinterpret_cast<WarpState<T>*>(smem_raw)[wid];
+    WarpState<T>& S = T::COOP     ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x]
+                      : T::GLOBAL ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x * T::WARPS + wid]
+                                  : reinterpret_cast<WarpState<T>*>(pd_smem)[wid];
+    if (T::COOP) {
+        if (threadIdx.x == 0) coop_job().min_v = P.coop_min_v;
+        __syncthreads();
+        if (wid != 0) {  // helper warps of a cooperative CTA
+            coop_worker<T>(S, wid, lane);
+            return;
+        }
+    }
     const int64_t total = P.list ? (int64_t)(*P.list_count) : P.count;
     Counters cnt = {0, 0, 0, 0, 0, 0, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
     const int gw = blockIdx.x * T::WARPS + wid;
@@ -1076,6 +1326,10 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
         for (int b = 0; b < BATCH && b0 + b < total; ++b) {
             int64_t idx = b0 + b;
             int s = P.list ? P.list[idx] : (int)(P.begin + idx);
+            if (tier < P.start_tier) {  // test knob: hand every cell to the next tier untouched
+                if (lane == 0) P.next_list[atom_add_g32(P.next_count, 1)] = s;
+                continue;
+            }
             Cell& c = S.c;
             const Counters before = cnt;
             float4 site = __ldg(&P.sites[s]);
@@ -1083,10 +1337,14 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             c.px = site.x; c.py = site.y; c.pz = site.z; c.pw = site.w;
             c.self = s;
             c.self_orig = __ldg(&P.perm[s]);
+            const long long t_cell = clock64();
             PT_BEGIN(t_init);
             init_cell(S, c, lane, P);
             PT_END(t_init, 0);
-            int st = traverse<T, MODE>(S, c, lane, P, cnt, spill, P.spill_cap);
+            int st = ST_OK;
+            if ((mode_flags<MODE>(P.flags) & PD_WARM_START) && P.knn) st = warm_start<T, MODE>(S, c, lane, P, cnt);
+            __syncwarp();
+            if (st == ST_OK) st = traverse<T, MODE>(S, c, lane, P, cnt, spill, P.spill_cap);
             __syncwarp();
             if (st == ST_OVERFLOW && !P.last_tier) {
                 if (lane == 0) {
@@ -1100,6 +1358,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             finalize(S, c, lane, P, st);
             PT_END(t_fin, 5);
             ncells++;
+            if (c.self_orig == P.trace_cell && lane == 0) trace_print(tier, c, cnt, before, st, clock64() - t_cell);
             if ((P.flags & PD_COST) && lane == 0) {  // deterministic work count (balanced cuts must agree)
                 unsigned long long w = (cnt.nodes - before.nodes) + (cnt.sites - before.sites) + 8 * (cnt.clips - before.clips);
                 P.out.cost[c.self_orig] = (int32_t)min(w, 0x7fffffffull);
@@ -1107,7 +1366,13 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             __syncwarp();
         }
     }
-    if ((P.flags & PD_STATS) && lane == 0) {
+    if (T::COOP) {  // release the helper warps
+        if (lane == 0) coop_job().kind = JOB_EXIT;
+        __syncwarp();
+        named_bar(1, T::WARPS * 32);
+    }
+    // counters of every tier, or only of tier $PD_PROF_TIER when it is set (per-tier profiles)
+    if ((P.flags & PD_STATS) && lane == 0 && (P.prof_tier < 0 || P.prof_tier == tier)) {
         red_add_g(&P.stats->nodes, cnt.nodes);
         red_add_g(&P.stats->leaves, cnt.leaves);
         red_add_g(&P.stats->sites, cnt.sites);
@@ -1117,14 +1382,16 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
         red_add_g(&P.stats->tier[tier], ncells);
         red_add_g(&P.stats->overflow, novf);
         red_add_g(&P.stats->spills, cnt.spills);
-        if (P.prof_tier < 0 || P.prof_tier == tier)
-            for (int k = 0; k < 10; ++k) red_add_g(&P.stats->cyc[k], cnt.cyc[k]);
+        for (int k = 0; k < 10; ++k) red_add_g(&P.stats->cyc[k], cnt.cyc[k]);
     }
 }
 
 template <class T, unsigned MODE>
 int tier_grid(int num_sms) {
-    if (T::GLOBAL) return num_sms * kTier3BlocksPerSM;
+    if (T::GLOBAL) {
+        if (T::COOP) cudaFuncSetAttribute(cells_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CoopJob));
+        return num_sms * kTier3BlocksPerSM;
+    }
     size_t smem = sizeof(WarpState<T>) * T::WARPS;
     cudaFuncSetAttribute(cells_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
@@ -1135,7 +1402,7 @@ int tier_grid(int num_sms) {
 
 template <class T, unsigned MODE>
 cudaError_t launch_tier(const CellParams& p, int tier, cudaStream_t st, int num_sms) {
-    size_t smem = T::GLOBAL ? 0 : sizeof(WarpState<T>) * T::WARPS;
+    size_t smem = T::COOP ? sizeof(CoopJob) : T::GLOBAL ? 0 : sizeof(WarpState<T>) * T::WARPS;
     int grid = tier_grid<T, MODE>(num_sms);
     cells_kernel<T, MODE><<<grid, T::WARPS * 32, smem, st>>>(p, tier);
     return cudaGetLastError();
@@ -1151,6 +1418,7 @@ cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num
             case PD_PAPER_BOUND: return launch_tier<Tier1, PD_PAPER_BOUND>(p, 0, st, num_sms);
             case PD_ISOTROPIC: return launch_tier<Tier1, PD_ISOTROPIC>(p, 0, st, num_sms);
             case PD_DFS: return launch_tier<Tier1, PD_DFS>(p, 0, st, num_sms);
+            case PD_WARM_START: return launch_tier<Tier1, PD_WARM_START>(p, 0, st, num_sms);
             default: return launch_tier<Tier1, kDynMode>(p, 0, st, num_sms);
         }
     }
@@ -1159,7 +1427,7 @@ cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num
 }
 
 size_t cells_global_state_bytes(int num_sms) {
-    return (size_t)tier_grid<Tier3, kDynMode>(num_sms) * Tier3::WARPS * sizeof(WarpState<Tier3>);
+    return (size_t)tier_grid<Tier3, kDynMode>(num_sms) * (Tier3::COOP ? 1 : Tier3::WARPS) * sizeof(WarpState<Tier3>);
 }
 
 int cells_grid_warps(int tier, int num_sms) {
@@ -1169,6 +1437,7 @@ int cells_grid_warps(int tier, int num_sms) {
         g = max(g, tier_grid<Tier1, PD_PAPER_BOUND>(num_sms));
         g = max(g, tier_grid<Tier1, PD_ISOTROPIC>(num_sms));
         g = max(g, tier_grid<Tier1, PD_DFS>(num_sms));
+        g = max(g, tier_grid<Tier1, PD_WARM_START>(num_sms));
         g = max(g, tier_grid<Tier1, kDynMode>(num_sms));
         return g * Tier1::WARPS;
     }

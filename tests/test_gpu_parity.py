@@ -96,12 +96,52 @@ def test_leaf_sizes_identical(leaf):
     assert np.allclose(ref.volumes, g.volumes, rtol=1e-6, atol=0)
 
 
-@pytest.mark.parametrize("flag", [pd.ISOTROPIC, pd.DFS, pd.PAPER_BOUND])
+@pytest.mark.parametrize("flag", [pd.ISOTROPIC, pd.DFS, pd.PAPER_BOUND, pd.WARM_START, pd.WARM_START | pd.DFS])
 def test_ablations_neutral(flag):
     """Culling / traversal variants change the work, not the diagram."""
     wl = pdgen.make("C3", n=8009)
     ref = _gpu(wl)
     g = _gpu(wl, flags=flag)
+    assert np.array_equal(ref.offsets, g.offsets) and np.array_equal(ref.neighbors, g.neighbors)
+    assert np.allclose(ref.volumes, g.volumes, rtol=1e-6)
+
+
+@pytest.mark.parametrize("cfg,n", [("C1", None), ("C3", 20011), ("C5", 20011)])
+def test_warm_start_parity(cfg, n):
+    """KNN warm start against the oracle, incl. weight-emptied and heavy cells, and
+    with a leaf of one site (KNN over single-site leaves)."""
+    _assert_parity(pdgen.make(cfg, n=n), flags=pd.WARM_START)
+    _assert_parity(pdgen.make(cfg, n=n), flags=pd.WARM_START, leaf_size=1)
+
+
+def test_warm_start_duplicates_and_lattice():
+    """Warm start with coincident sites (excluded from the KNN; the leaf processing decides ownership)
+    and with cospherical lattices (KNN planes met again in their leaves must not re-clip)."""
+    pts = np.array([[0.5, 0.5, 0.5], [0.25, 0.5, 0.5], [0.5, 0.5, 0.5], [0.75, 0.5, 0.5], [0.5, 0.5, 0.5]], np.float32)
+    box = (0, 0, 0, 1, 1, 1)
+    a = pd.build_diagram(pts, None, box, out_host=True)
+    b = pd.build_diagram(pts, None, box, out_host=True, flags=pd.WARM_START)
+    for k in ("offsets", "neighbors", "flags"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    gr = np.arange(-3, 4, dtype=np.float64)
+    P = (np.stack(np.meshgrid(gr, gr, gr, indexing="ij"), -1).reshape(-1, 3) * 0.5).astype(np.float32)
+    a = pd.build_diagram(P, None, (-1.8,) * 3 + (1.8,) * 3, out_host=True)
+    b = pd.build_diagram(P, None, (-1.8,) * 3 + (1.8,) * 3, out_host=True, flags=pd.WARM_START)
+    assert np.array_equal(a.offsets, b.offsets) and np.array_equal(a.neighbors, b.neighbors)
+    assert np.allclose(a.volumes, b.volumes, rtol=1e-6)
+
+
+@pytest.mark.parametrize("cfg,n", [("C3", 6007), ("C5", 6007)])
+@pytest.mark.parametrize("flags", [0, pd.WARM_START])
+def test_top_tier_cooperative(cfg, n, flags, monkeypatch):
+    """Every cell through the top capacity tier (state in global memory, one cell per CTA) with every
+    O(V) pass CTA-cooperative (classification, exact node tests, AABB, twins, face areas): parity with
+    the oracle and the same neighbour sets as the default tiers."""
+    wl = pdgen.make(cfg, n=n)
+    ref = _gpu(wl, flags=flags)
+    monkeypatch.setenv("PD_START_TIER", "2")
+    monkeypatch.setenv("PD_COOP_MIN_V", "0")
+    g, o, rep = _assert_parity(wl, flags=flags | pd.STATS)
     assert np.array_equal(ref.offsets, g.offsets) and np.array_equal(ref.neighbors, g.neighbors)
     assert np.allclose(ref.volumes, g.volumes, rtol=1e-6)
 

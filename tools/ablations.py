@@ -13,7 +13,7 @@ import pdgen  # noqa: E402
 import paper_2605_06408_b200 as pd  # noqa: E402
 
 MODES = {"default": 0, "paper_bound": pd.PAPER_BOUND, "isotropic": pd.ISOTROPIC, "dfs": pd.DFS,
-         "no_exact": pd.NO_EXACT}
+         "no_exact": pd.NO_EXACT, "warm_start": pd.WARM_START}
 cfgs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C2", "C3", "C4"]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1_000_000
 for cfg in cfgs:
