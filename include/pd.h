@@ -65,8 +65,10 @@ enum {
     PD_COST = 1u << 7,        /* record per-cell work (pd_cell_cost): BVH nodes + leaf sites + 8 x clips (deterministic) */
     PD_EXACT_NODES = 1u << 8, /* exact polytope-vs-box node test on every node the AABB tests keep */
     PD_NO_EXACT = 1u << 9,    /* never use the exact polytope-vs-box node test (pure AABB culling) */
-    PD_BALANCE = 1u << 10     /* sharded build: equal-cost Morton slices from a sampled cost estimate
+    PD_BALANCE = 1u << 10,    /* sharded build: equal-cost Morton slices from a sampled cost estimate
                                  (default: equal-count slices, measured better balanced on C4) */
+    PD_TETS = 1u << 11        /* also output the dual tetrahedra (the "explicit mesh"
+                                 of PAPER.md:343/398): see pd_tets.  Not with shard_world > 1 (PD_EINVAL). */
 };
 
 /* pd_cell_flags values */
@@ -130,6 +132,15 @@ const float* pd_volumes(const pd_result* r);     /* n; 0 for EMPTY */
 const float* pd_surface(const pd_result* r);     /* n; total surface area incl. box walls */
 const uint8_t* pd_cell_flags(const pd_result* r);/* n; PD_CELL_* bits */
 const int32_t* pd_cell_cost(const pd_result* r); /* n (device); per-cell work count, only with PD_COST, else NULL */
+/* Dual tetrahedra (PD_TETS): the regular (weighted Delaunay) triangulation dual to the diagram, restricted
+ * to the box.  Every cell vertex where three bisector faces of positive area meet (no box wall) is the
+ * centre of the tet {i, a, b, c} (the vertex is equidistant in power from the four
+ * sites); each tet is listed once, by its lowest id i.  pd_tets: 4*pd_num_tets int32 original ids,
+ * (i < a < b < c) per tet, grouped by i ascending, within a group in the emitting cell's vertex order.
+ * NULL / 0 without PD_TETS.  Near-degenerate (cospherical) configurations may list sliver tets
+ * of zero volume: the triplet dual splits a vertex of degree > 3. */
+int64_t pd_num_tets(const pd_result* r);
+const int32_t* pd_tets(const pd_result* r);
 pd_status pd_get_stats(const pd_result* r, pd_stats* s);
 void pd_free(pd_result* r);
 

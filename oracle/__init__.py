@@ -136,3 +136,43 @@ def cell_geometry(points, weights, box, i: int, order_k: int = 64,
         loops.append(xyz[o:o + nv[f]].copy())
         o += nv[f]
     return CellGeometry(tags[:nf].copy(), loops, planes[:nf].copy(), int(fl[0]))
+
+
+def dual_tets(points, weights, box, ids=None, order_k: int = 64):
+    """Dual tetrahedra of the diagram in the box (the "explicit mesh" of
+    PAPER.md:343, 398): for each requested cell i, every vertex v of K_i (the same point in several
+    of the oracle's face loops -- the clipper builds shared points bit-identically) is a corner where
+    the faces tagged T(v) meet.  If T(v) is exactly three bisector faces {a, b, c} of area
+    > 1e-13 S_i (reading R2; no wall), v is power-equidistant from p_i, p_a, p_b, p_c and
+    no site is closer, so {i, a, b, c} is a tet of the regular triangulation.
+    Each tet is reported once, by its lowest id.  Returns (int64 [T, 4] rows (i<a<b<c) sorted
+    lexicographically, number of vertices where more than three faces meet (degenerate, skipped)).
+    Pinned by tests/test_oracle_pins.py::test_dual_tets_* (scipy Delaunay / lifted Qhull)."""
+    n = len(points)
+    out, ndeg = [], 0
+    for i in (range(n) if ids is None else ids):
+        g = cell_geometry(points, weights, box, int(i), order_k)
+        if not g.loops:
+            continue
+        areas = []
+        for lp in g.loops:
+            A = 0.5 * np.sum(np.cross(lp, np.roll(lp, -1, axis=0)), axis=0)
+            areas.append(float(np.sqrt(A @ A)))
+        amin = 1e-13 * sum(areas)
+        at = {}
+        for f, lp in enumerate(g.loops):
+            for v in lp:
+                at.setdefault((v[0], v[1], v[2]), set()).add(f)
+        for fs in at.values():
+            if len(fs) > 3:
+                ndeg += 1
+                continue
+            if len(fs) < 3:
+                continue
+            tags = sorted(int(g.tags[f]) for f in fs)
+            if tags[0] < 0 or any(areas[f] <= amin for f in fs):
+                continue
+            if int(i) < tags[0]:
+                out.append((int(i), tags[0], tags[1], tags[2]))
+    t = np.array(sorted(out), dtype=np.int64).reshape(-1, 4)
+    return t, ndeg

@@ -23,14 +23,14 @@ LIB_PATH = os.path.join(HERE, "libpd.so")
 PD_OK, PD_EINVAL, PD_EEMPTY, PD_ENONFINITE, PD_EOUTSIDE, PD_ENOMEM, PD_ECUDA, PD_ENCCL, PD_EINTERNAL = range(9)
 IN_DEVICE, OUT_HOST, STATS, ISOTROPIC, DFS, PAPER_BOUND, COST, EXACT_NODES, NO_EXACT, BALANCE = (
     1, 2, 4, 8, 16, 64, 128, 256, 512, 1024)
-WARM_START = 32
+WARM_START, TETS = 32, 2048
 CELL_EMPTY, CELL_BOUNDARY, CELL_OVERFLOW, CELL_DUPLICATE, CELL_NOT_OWNED = 1, 2, 4, 8, 32
 
 EXPORTED = ["pd_build", "pd_num_cells", "pd_nnz", "pd_on_host", "pd_offsets", "pd_neighbors", "pd_face_areas",
             "pd_volumes", "pd_surface", "pd_cell_flags", "pd_cell_cost", "pd_get_stats", "pd_free", "pd_slice_begin",
             "pd_slice_end", "pd_morton_perm", "pd_assemble", "pd_export_slice", "pd_slice_nnz",
             "pd_strerror", "pd_error_index", "pd_last_cuda_error", "pd_abi_version", "pd_last_launch_count",
-            "pd_sort_pairs_u64"]
+            "pd_sort_pairs_u64", "pd_num_tets", "pd_tets"]
 
 
 class PdError(RuntimeError):
@@ -101,6 +101,11 @@ def load_library(path: str | None = None):
     L.pd_last_cuda_error.restype = ctypes.c_char_p
     L.pd_abi_version.restype = ctypes.c_int
     L.pd_last_launch_count.restype = I64
+    if hasattr(L, "pd_tets"):
+        L.pd_num_tets.restype = I64
+        L.pd_num_tets.argtypes = [P]
+        L.pd_tets.restype = P
+        L.pd_tets.argtypes = [P]
     if hasattr(L, "pd_sort_pairs_u64"):  # optional test hook (absent in older A/B builds)
         L.pd_sort_pairs_u64.restype = ctypes.c_int
         L.pd_sort_pairs_u64.argtypes = [P, P, I64, P, P, P]
@@ -164,6 +169,7 @@ class Diagram:
     handle: object = None
     slice_begin: int = 0
     slice_end: int = 0
+    tets: object = None  # int32 [ntets, 4] with flags=TETS (pd_tets), else None
 
     def row(self, i):
         a, b = int(self.offsets[i]), int(self.offsets[i + 1])
@@ -175,7 +181,7 @@ class Diagram:
         cv = lambda t: t.cpu().numpy()
         return Diagram(self.n, self.nnz, cv(self.offsets), cv(self.neighbors), cv(self.areas), cv(self.volumes),
                        cv(self.surface), cv(self.flags), self.stats, True, self.handle, self.slice_begin,
-                       self.slice_end)
+                       self.slice_end, None if self.tets is None else cv(self.tets))
 
 
 def _wrap(ptr, stream_ptr) -> Diagram:
@@ -204,6 +210,15 @@ def _wrap(ptr, stream_ptr) -> Diagram:
             arrs[k] = torch.as_tensor(_CudaView(h, ptrs[k], (size,), tstr), device="cuda")
     d = Diagram(n, nnz, arrs["offsets"], arrs["neighbors"], arrs["areas"], arrs["volumes"], arrs["surface"],
                 arrs["flags"], st.as_dict(), on_host, h, int(L.pd_slice_begin(ptr)), int(L.pd_slice_end(ptr)))
+    tp = L.pd_tets(ptr) if hasattr(L, "pd_tets") else None
+    if tp:
+        nt = int(L.pd_num_tets(ptr))
+        if on_host:
+            buf = (ctypes.c_char * max(nt * 16, 1)).from_address(tp)
+            d.tets = np.frombuffer(buf, dtype=np.int32, count=nt * 4).reshape(nt, 4)
+        else:
+            import torch
+            d.tets = torch.as_tensor(_CudaView(h, tp, (nt, 4), "<i4"), device="cuda")
     return d
 
 

@@ -26,6 +26,8 @@ struct pd_result {
     int64_t* offsets = nullptr;
     int32_t* nbr = nullptr;
     float* area = nullptr;
+    int64_t ntets = 0;
+    int32_t* tets = nullptr;  // PD_TETS: 4 * ntets
     float* vol = nullptr;
     float* surf = nullptr;
     uint8_t* flags = nullptr;
@@ -210,6 +212,7 @@ void finish_outputs(pd_result* r, Arena& A, unsigned flags, cudaStream_t st) {
         r->vol = host_copy(r, r->vol, (size_t)r->n, st);
         r->surf = host_copy(r, r->surf, (size_t)r->n, st);
         r->flags = host_copy(r, r->flags, (size_t)r->n, st);
+        if (r->tets) r->tets = host_copy(r, r->tets, (size_t)r->ntets * 4, st);
         r->on_host = 1;
     }
     (void)A;
@@ -232,6 +235,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
     int world = opt.shard_world > 1 ? opt.shard_world : 1;
     int rank = world > 1 ? opt.shard_rank : 0;
     if (rank < 0 || rank >= world) return PD_EINVAL;
+    if ((opt.flags & PD_TETS) && world > 1) return PD_EINVAL;
     g_launches = 0;
     int launches = 0;
     ck(cudaSetDevice(opt.device));
@@ -441,8 +445,19 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         float* aarea = nullptr;
         cudaEvent_t tev[4];
         for (auto& e : tev) ck(cudaEventCreate(&e));
+        // dual tetrahedra (PD_TETS): ~6.8 per site for Poisson-Voronoi input, each listed once
+        const bool want_tets = (opt.flags & PD_TETS) != 0;
+        int32_t* tcnt = want_tets ? W.alloc<int32_t>(n) : nullptr;
+        int64_t* taoff = want_tets ? W.alloc<int64_t>(n) : nullptr;
+        int* tovf = want_tets ? W.alloc<int>(1) : nullptr;
+        int4* tarena = nullptr;
+        int64_t tcap = std::max<int64_t>((end - begin) * 8, 4096);
         for (int attempt = 0; attempt < 3; ++attempt) {
             anbr = W.alloc<int32_t>(cap);
+            if (want_tets) {
+                tarena = W.alloc<int4>(tcap);
+                ck(cudaMemsetAsync(tovf, 0, sizeof(int), st));
+            }
             nbr = A.alloc<int32_t>(cap);
             area = A.alloc<float>(cap);
             aarea = W.alloc<float>(cap);
@@ -475,6 +490,14 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.out.arena_cap = cap;
             P.out.arena_overflow = aovf;
             P.out.cost = cost;
+            if (want_tets) {
+                P.out.tcnt = tcnt;
+                P.out.taoff = taoff;
+                P.out.tarena = tarena;
+                P.out.ttop = counters + 5;
+                P.out.tcap = tcap;
+                P.out.tovf = tovf;
+            }
             P.stats = dstats;
             P.spill = spill;
             P.gstate = gstate;
@@ -504,14 +527,19 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
                 ck(pd::launch_cells(tier, P, st, sms, &launches));
             }
             ck(cudaEventRecord(tev[3], st));
-            unsigned long long top = 0;
-            int ovf = 0;
+            unsigned long long top = 0, ttop = 0;
+            int ovf = 0, t_ovf = 0;
             ck(cudaMemcpyAsync(&top, counters + 4, sizeof(top), cudaMemcpyDeviceToHost, st));
             ck(cudaMemcpyAsync(&ovf, aovf, sizeof(ovf), cudaMemcpyDeviceToHost, st));
+            if (want_tets) {
+                ck(cudaMemcpyAsync(&ttop, counters + 5, sizeof(ttop), cudaMemcpyDeviceToHost, st));
+                ck(cudaMemcpyAsync(&t_ovf, tovf, sizeof(t_ovf), cudaMemcpyDeviceToHost, st));
+            }
             ck(cudaStreamSynchronize(st));
-            if (!ovf) break;
+            if (!ovf && !t_ovf) break;
             if (attempt == 2) throw Fail{PD_EINTERNAL};
-            cap = (int64_t)(top * 1.1) + 1024;  // rerun with an arena large enough
+            if (ovf) cap = (int64_t)(top * 1.1) + 1024;  // rerun with an arena large enough
+            if (t_ovf) tcap = (int64_t)(ttop * 1.1) + 1024;
         }
         ck(cudaEventRecord(ev[2], st));
         // ---- a13 CSR
@@ -525,6 +553,20 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         ck(cudaStreamSynchronize(st));
         if (nnz > cap) throw Fail{PD_EINTERNAL};
         ck(pd::csr_gather(cnt, aoff, offsets, anbr, aarea, n, nbr, area, st, &launches));
+        if (want_tets) {  // dual tetrahedra rows in original-id order (same scan + gather as the CSR)
+            int64_t* toff = W.alloc<int64_t>((size_t)n + 1);
+            size_t tb2 = 0;
+            ck(pd::scan_counts(tcnt, toff, n, nullptr, &tb2, st, nullptr));
+            void* ttmp = W.alloc<unsigned char>(tb2);
+            ck(pd::scan_counts(tcnt, toff, n, ttmp, &tb2, st, &launches));
+            int64_t nt = 0;
+            ck(cudaMemcpyAsync(&nt, toff + n, sizeof(nt), cudaMemcpyDeviceToHost, st));
+            ck(cudaStreamSynchronize(st));
+            int4* tt = A.alloc<int4>((size_t)std::max<int64_t>(nt, 1));
+            ck(pd::tet_gather(tcnt, taoff, toff, tarena, n, tt, st, &launches));
+            r->ntets = nt;
+            r->tets = (int32_t*)to_result(r, A, tt);
+        }
         ck(cudaEventRecord(ev[3], st));
         r->nnz = nnz;
         r->offsets = to_result(r, A, offsets);
@@ -612,6 +654,8 @@ const float* pd_volumes(const pd_result* r) { return r ? r->vol : nullptr; }
 const float* pd_surface(const pd_result* r) { return r ? r->surf : nullptr; }
 const uint8_t* pd_cell_flags(const pd_result* r) { return r ? r->flags : nullptr; }
 const int32_t* pd_cell_cost(const pd_result* r) { return r ? r->cost : nullptr; }
+int64_t pd_num_tets(const pd_result* r) { return r ? r->ntets : 0; }
+const int32_t* pd_tets(const pd_result* r) { return r ? r->tets : nullptr; }
 pd_status pd_get_stats(const pd_result* r, pd_stats* s) {
     if (!r || !s) return PD_EINVAL;
     *s = r->stats;

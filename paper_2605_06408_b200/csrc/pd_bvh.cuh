@@ -41,6 +41,10 @@ cudaError_t scan_counts(const int32_t* cnt, int64_t* offsets, int64_t n, void* t
 cudaError_t csr_gather(const int32_t* cnt, const int64_t* aoff, const int64_t* offsets, const int32_t* arena_nbr,
                        const float* arena_area, int64_t n, int32_t* nbr, float* area, cudaStream_t st, int* launches);
 
+// dual tetrahedra rows: copy each cell's arena tets into the final order
+cudaError_t tet_gather(const int32_t* tcnt, const int64_t* taoff, const int64_t* toff, const int4* tarena, int64_t n,
+                       int4* tets, cudaStream_t st, int* launches);
+
 // sharding helpers
 cudaError_t slice_export_meta(const int32_t* perm, int64_t begin, int64_t len, const int32_t* cnt, const float* vol,
                               const float* surf, const uint8_t* flags, int32_t* cnt_m, float* vol_m, float* surf_m,

@@ -65,11 +65,13 @@ constexpr unsigned FULL = 0xffffffffu;
 #define PD_EDGE_BITMAP 0
 #endif
 
-template <int V, int P, int Q, int W, int MINB, bool GLOB = false, bool CO = false>
+template <int V, int P, int Q, int W, int MINB, bool GLOB = false, bool CO = false, bool SPH = false>
 struct TierCfg {
     static constexpr bool GLOBAL = GLOB;     // warp state in global memory (top tier) instead of smem
     // CTA-cooperative cell (top tier): warp 0 runs the cell program, warps 1..W-1 join its O(V) passes
     static constexpr bool COOP = CO;
+    // bounding-sphere companion of the site cull (tiers whose cells grow large; see site_culled)
+    static constexpr bool SPHERE = SPH;
     using trip_t = typename std::conditional<(P <= 1024), uint32_t, uint64_t>::type;
     static constexpr int VMAX = V;   // vertices
     static constexpr int PMAX = P;   // planes (<= 1024: 10-bit triplet fields)
@@ -95,8 +97,11 @@ struct TierCfg {
 #ifndef PD_T1_P
 #define PD_T1_P 64
 #endif
-using Tier1 = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, 4, PD_T1_MINB>;
-using Tier2 = TierCfg<384, 192, 256, 4, 1>;
+#ifndef PD_T1_SPHERE
+#define PD_T1_SPHERE 0
+#endif
+using Tier1 = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, 4, PD_T1_MINB, false, false, PD_T1_SPHERE != 0>;
+using Tier2 = TierCfg<384, 192, 256, 4, 1, false, false, true>;
 // Top tier: state in global memory (L1/L2-cached), 64-bit plane-index triplets; for the rare cells
 // with thousands of faces (heavy-tailed weights, SURVEY.md §7 hard part 3).
 // One cell per CTA: its 16 warps share every O(V) pass (classification, exact node tests, AABB,
@@ -107,7 +112,7 @@ using Tier2 = TierCfg<384, 192, 256, 4, 1>;
 #ifndef PD_T3_WARPS
 #define PD_T3_WARPS 16
 #endif
-using Tier3 = TierCfg<16384, 8192, 4096, PD_T3_COOP ? PD_T3_WARPS : 2, 1, true, PD_T3_COOP != 0>;
+using Tier3 = TierCfg<16384, 8192, 4096, PD_T3_COOP ? PD_T3_WARPS : 2, 1, true, PD_T3_COOP != 0, true>;
 constexpr int kTier3BlocksPerSM = 1;
 
 // Per-warp cell state (warp-uniform).  Lives in the warp's shared-memory block (read by broadcast):
@@ -119,6 +124,7 @@ struct Cell {
     float flo[3], fhi[3];   // cell AABB, site-local, rounded outward
     float vmax;             // max_k max(|lo_k|, |hi_k|)
     float rmax;             // max corner distance of the AABB (isotropic radius bound)
+    float sc[3], srad;      // bounding sphere of the cell (SPHERE tiers): center (site-local), radius
     int nv, np, nq;
     int self;               // Morton index
     int self_orig;
@@ -308,7 +314,8 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
 // meets warps 1..W-1 at named barrier 1, every warp takes a strided share of the vertex (or face)
 // slots, and all meet again at barrier 2, after which warp 0 combines the per-warp partials in a fixed
 // order (so the result is deterministic).
-enum { JOB_EXIT = 0, JOB_CLASSIFY = 1, JOB_EXACT = 2, JOB_AABB = 3, JOB_TWINS = 4, JOB_AREAS = 5 };
+enum { JOB_EXIT = 0, JOB_CLASSIFY = 1, JOB_EXACT = 2, JOB_AABB = 3, JOB_TWINS = 4, JOB_AREAS = 5, JOB_BATCH = 6,
+       JOB_REVAL = 7 };
 constexpr int kCoopMaxW = 32;
 struct CoopJob {
     int kind, nv, np;
@@ -320,11 +327,24 @@ struct CoopJob {
     float4 lo[WIDE], hi[WIDE];
     int ipart[kCoopMaxW][WIDE];
     double dpart[kCoopMaxW][2];
+    unsigned flags;     // JOB_REVAL: culling mode
+    int nq;             // JOB_REVAL: queue length
+    float4 cD[32];      // JOB_BATCH: candidate planes (D, d) of a leaf, lane = candidate
+    float cm[32];       //            and their FP32 certification margins
 };
 extern __shared__ __align__(16) unsigned char pd_smem[];
 __device__ __forceinline__ CoopJob& coop_job() { return *reinterpret_cast<CoopJob*>(pd_smem); }
 template <class T>
 __device__ __forceinline__ int P_coop_min_v(const WarpState<T>&) { return coop_job().min_v; }
+// Cooperative tier: the priority queue lives in shared memory after the job record.
+template <class T>
+__device__ __forceinline__ float4* coop_queue_lo() { return reinterpret_cast<float4*>(pd_smem + ((sizeof(CoopJob) + 15) & ~15)); }
+template <class T>
+__device__ __forceinline__ float4* coop_queue_hi() { return coop_queue_lo<T>() + T::QMAX; }
+template <class T>
+__device__ __forceinline__ uint32_t* coop_queue_mask() { return reinterpret_cast<uint32_t*>(coop_queue_hi<T>() + T::QMAX); }
+template <class T>
+constexpr size_t coop_smem_bytes() { return ((sizeof(CoopJob) + 15) & ~(size_t)15) + 2 * sizeof(float4) * T::QMAX + 4 * T::QC; }
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -419,22 +439,42 @@ __device__ __forceinline__ void finish_aabb(Cell& c, const Box6& b) {
     c.vmax = vm;
 }
 
+// Cell AABB (and, in SPHERE tiers, a bounding sphere centred at the previous AABB's centre: any
+// fixed centre gives a valid sphere, and the previous box is known before the pass).
 template <class T>
 __device__ PD_INL_AABB void update_aabb(const WarpState<T>& S, Cell& c, int lane) {
     Box6 b;
     b.reset();
+    float m0 = 0.f, m1 = 0.f, m2 = 0.f, r2 = 0.f;
+    if (T::SPHERE) {
+        m0 = 0.5f * (c.flo[0] + c.fhi[0]); m1 = 0.5f * (c.flo[1] + c.fhi[1]); m2 = 0.5f * (c.flo[2] + c.fhi[2]);
+    }
     if (T::COOP && c.nv >= P_coop_min_v(S)) {
         CoopJob& J = coop_job();
-        if (lane == 0) { J.kind = JOB_AABB; J.nv = c.nv; }
+        if (lane == 0) { J.kind = JOB_AABB; J.nv = c.nv; J.lo[0] = make_float4(m0, m1, m2, 0.f); }
         coop_go<T>(const_cast<WarpState<T>&>(S), J, lane);
         if (lane < T::WARPS) {
             b.lo0 = iford(J.ipart[lane][0]); b.lo1 = iford(J.ipart[lane][1]); b.lo2 = iford(J.ipart[lane][2]);
             b.hi0 = iford(J.ipart[lane][3]); b.hi1 = iford(J.ipart[lane][4]); b.hi2 = iford(J.ipart[lane][5]);
+            r2 = iford(J.ipart[lane][6]);
         }
     } else {
-        for (int s = lane; s < c.nv; s += 32) b.add(S.fv[s]);
+        for (int s = lane; s < c.nv; s += 32) {
+            const float4 v = S.fv[s];
+            b.add(v);
+            if (T::SPHERE) {
+                const float dx = v.x - m0, dy = v.y - m1, dz = v.z - m2;
+                r2 = fmaxf(r2, dx * dx + dy * dy + dz * dz);
+            }
+        }
     }
+    if (T::SPHERE) r2 = iford(__reduce_max_sync(FULL, ford(r2)));
     finish_aabb(c, b);
+    if (T::SPHERE) {
+        // FP32 vertex copies are within 2^-24 |v| of the FP64 cell: 1e-6 vmax covers it
+        c.sc[0] = m0; c.sc[1] = m1; c.sc[2] = m2;
+        c.srad = sqrtf(r2) * (1.f + 1e-6f) + 1e-6f * c.vmax;
+    }
 }
 
 __device__ __forceinline__ void put_vertex(float4* fv, double* vx, double* vy, double* vz, int s, double x, double y, double z) {
@@ -717,6 +757,9 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
 // cannot cut the cell.  Paper: d_ij = q/(2|D|) > r with r the directional radius of p_j's octant.
 // Default: the exact support of the cell AABB in direction D, h = sum_k max(lo_k D_k, hi_k D_k)
 // <= r |D| (Cauchy-Schwarz), cull iff q/2 > h: never looser.  Margins only ever keep a site.
+// SPHERE tiers also bound the support by the cell's bounding sphere, h <= m.D + rho |D|: much tighter
+// than the box for the huge, round cells of heavy sites, whose AABB holds thousands of candidates.
+template <bool SPH>
 __device__ __forceinline__ bool site_culled(const Cell& c, float Dx, float Dy, float Dz, float D2, float dq,
                                             unsigned flags) {
     const float q = D2 + dq;
@@ -724,6 +767,11 @@ __device__ __forceinline__ bool site_culled(const Cell& c, float Dx, float Dy, f
         float h = Dx * (Dx >= 0.f ? c.fhi[0] : c.flo[0]) + Dy * (Dy >= 0.f ? c.fhi[1] : c.flo[1]) +
                   Dz * (Dz >= 0.f ? c.fhi[2] : c.flo[2]);
         float mag = c.vmax * (fabsf(Dx) + fabsf(Dy) + fabsf(Dz));
+        if (SPH) {
+            const float rd = c.srad * sqrtf(D2);
+            h = fminf(h, fmaf(c.sc[0], Dx, fmaf(c.sc[1], Dy, c.sc[2] * Dz)) + rd);
+            mag += rd;
+        }
         return 0.5f * q - h > 1e-5f * (D2 + fabsf(dq) + mag);
     }
     float r2;
@@ -770,7 +818,7 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
     }
     if (__any_sync(FULL, dup_kill)) return ST_DUP;
     cnt.sites += count;
-    bool cand = valid && !site_culled(c, Dx, Dy, Dz, D2, dq, flags);
+    bool cand = valid && !site_culled<T::SPHERE>(c, Dx, Dy, Dz, D2, dq, flags);
     unsigned mask = __ballot_sync(FULL, cand);
     if (!mask) return ST_OK;
     // Batch cut test, lane = candidate: does the plane cut the CURRENT cell?  A plane that does not
@@ -794,7 +842,24 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         cand = cand && cuts;
         mask = __ballot_sync(FULL, cand);
     }
-    if (!PD_BATCH_CUT) cnt.tests += __popc(mask);
+    bool batched = PD_BATCH_CUT;
+    if (T::COOP && !PD_BATCH_CUT && c.nv >= P_coop_min_v(S) && (mask & (mask - 1))) {
+        // cooperative tier: one CTA-wide pass tests every candidate of the leaf against the current
+        // cell (same certified predicate); only the planes that cut go on to clip()
+        CoopJob& J = coop_job();
+        if (cand) { J.cD[lane] = make_float4(Dx, Dy, Dz, dd); J.cm[lane] = m; }
+        if (lane == 0) { J.kind = JOB_BATCH; J.nv = c.nv; J.mask = mask; }
+        coop_go<T>(S, J, lane);
+        unsigned cut = 0u, amb = 0u;
+        for (int w = 0; w < T::WARPS; ++w) { cut |= (unsigned)J.ipart[w][0]; amb |= (unsigned)J.ipart[w][1]; }
+        bool cuts = (cut >> lane) & 1u;
+        if (cand && !cuts && ((amb >> lane) & 1u)) cuts = cuts_fp64(S, c, sj, D2);  // certify in FP64 (rare)
+        cnt.tests += __popc(mask);
+        cand = cand && cuts;
+        mask = __ballot_sync(FULL, cand);
+        batched = true;
+    }
+    if (!batched) cnt.tests += __popc(mask);
     float key = cand ? dd * rsqrtf(D2) : INFINITY;  // d_ij: nearest plane first
     while (mask) {
         int kmin = __reduce_min_sync(FULL, cand ? ford(key) : 0x7fffffff);
@@ -816,7 +881,7 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         if (st == CLIP_OVF) return ST_OVERFLOW;
         if (st == CLIP_DONE) {
             cnt.clips++;
-            if (cand && site_culled(c, Dx, Dy, Dz, D2, dq, flags)) cand = false;
+            if (cand && site_culled<T::SPHERE>(c, Dx, Dy, Dz, D2, dq, flags)) cand = false;
         }
         mask = __ballot_sync(FULL, cand);
     }
@@ -847,6 +912,10 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                         int spill_cap) {
     const unsigned flags = mode_flags<MODE>(P.flags);
     const bool dfs = (flags & PD_DFS) != 0;
+    // the queue: in the warp's state, or (cooperative top tier, state in global memory) in shared memory
+    float4* const qlo = T::COOP ? coop_queue_lo<T>() : S.qlo;
+    float4* const qhi = T::COOP ? coop_queue_hi<T>() : S.qhi;
+    uint32_t* const qmask = T::COOP ? coop_queue_mask<T>() : S.qmask;
     int node = __float_as_int(__ldg(&P.root->hi_l.w));
     bool have = true;
     int ns = 0;  // spilled entries
@@ -915,8 +984,8 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     if (push) {
                         if (rank < room) {
                             if (PD_LAZY_POP) S.qkey[nq + rank] = key;
-                            S.qlo[nq + rank] = lo_w;
-                            S.qhi[nq + rank] = hi_l;
+                            qlo[nq + rank] = lo_w;
+                            qhi[nq + rank] = hi_l;
                         } else {
                             spill[ns + rank - room].lo_w = lo_w;
                             spill[ns + rank - room].hi_l = hi_l;
@@ -950,8 +1019,8 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     bool cu;
                     S.qkey[t] = node_test(c, e.lo_w, e.hi_l, flags, cu);
                 }
-                S.qlo[t] = e.lo_w;
-                S.qhi[t] = e.hi_l;
+                qlo[t] = e.lo_w;
+                qhi[t] = e.hi_l;
             }
             ns -= mm;
             nq = mm;
@@ -963,8 +1032,8 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             while (nq > 0 && !ok) {
                 int t = nq - 1;
                 bool culled;
-                node_test(c, S.qlo[t], S.qhi[t], flags, culled);
-                node = __float_as_int(S.qhi[t].w);
+                node_test(c, qlo[t], qhi[t], flags, culled);
+                node = __float_as_int(qhi[t].w);
                 nq--;
                 ok = !culled;
             }
@@ -986,11 +1055,11 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             }
             int gk = __reduce_min_sync(FULL, bk);
             int bslot = __shfl_sync(FULL, bs, __ffs(__ballot_sync(FULL, bk == gk)) - 1);
-            float4 lo = S.qlo[bslot], hi = S.qhi[bslot];
+            float4 lo = qlo[bslot], hi = qhi[bslot];
             __syncwarp();
             if (lane == 0 && bslot != nq - 1) {
-                S.qlo[bslot] = S.qlo[nq - 1];
-                S.qhi[bslot] = S.qhi[nq - 1];
+                qlo[bslot] = qlo[nq - 1];
+                qhi[bslot] = qhi[nq - 1];
                 S.qkey[bslot] = S.qkey[nq - 1];
             }
             --nq;
@@ -1007,17 +1076,29 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         }
         int bestk = 0x7fffffff, bests = -1;
         const int qch = (nq + 31) >> 5;
+        int alive_total = -1;
+        if (T::COOP && nq >= 8 * 32) {  // the whole CTA re-validates a long queue
+            CoopJob& J = coop_job();
+            if (lane == 0) { J.kind = JOB_REVAL; J.nq = nq; J.flags = flags; }
+            coop_go<T>(S, J, lane);
+            const int k = lane < T::WARPS ? J.ipart[lane][0] : 0x7fffffff;
+            const int sl = lane < T::WARPS ? J.ipart[lane][1] : 0x7fffffff;
+            const int g = __reduce_min_sync(FULL, k);
+            bestk = g;
+            bests = __reduce_min_sync(FULL, k == g ? sl : 0x7fffffff);
+            alive_total = __reduce_add_sync(FULL, lane < T::WARPS ? J.ipart[lane][2] : 0);
+        } else
         for (int ch = 0; ch < qch; ++ch) {
             int s = ch * 32 + lane;
             bool al = false;
             if (s < nq) {
                 bool culled;
-                float k = node_test(c, S.qlo[s], S.qhi[s], flags, culled);
+                float k = node_test(c, qlo[s], qhi[s], flags, culled);
                 al = !culled;
                 if (al && ford(k) < bestk) { bestk = ford(k); bests = s; }
             }
             unsigned am = __ballot_sync(FULL, al);
-            if (lane == 0) S.qmask[ch] = am;
+            if (lane == 0) qmask[ch] = am;
         }
         __syncwarp();
         int gk = __reduce_min_sync(FULL, bestk);
@@ -1029,23 +1110,35 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         }
         unsigned lead = __ballot_sync(FULL, bestk == gk);
         int bslot = __shfl_sync(FULL, bests, __ffs(lead) - 1);
-        node = __float_as_int(S.qhi[bslot].w);
+        node = __float_as_int(qhi[bslot].w);
         bool popped_dead = (exact_on(flags, cnt.nodes - nodes0, P.exact_after) ||
                             (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) && node < 0)) &&
-                           node_exact_culled(S, c, lane, S.qlo[bslot], S.qhi[bslot]);
+                           node_exact_culled(S, c, lane, qlo[bslot], qhi[bslot]);
+        if (T::COOP && alive_total * 4 > nq * 3) {
+            // mostly alive: remove only the popped entry (the last one fills its slot);
+            // the few dead entries stay and are found dead again (culling is monotone), until a
+            // re-validation finds a quarter of the queue dead and compacts it below
+            __syncwarp();
+            if (lane == 0 && bslot != nq - 1) { qlo[bslot] = qlo[nq - 1]; qhi[bslot] = qhi[nq - 1]; }
+            __syncwarp();
+            nq -= 1;
+            have = !popped_dead;
+            PT_END(t_pop, 4);
+            continue;
+        }
         // compact: keep alive entries except the popped one
         int base = 0;
         for (int ch = 0; ch < qch; ++ch) {
             int s = ch * 32 + lane;
-            bool keep = ((S.qmask[ch] >> lane) & 1u) && s != bslot;
+            bool keep = ((qmask[ch] >> lane) & 1u) && s != bslot;
             unsigned km = __ballot_sync(FULL, keep);
             float4 lo = make_float4(0, 0, 0, 0), hi = make_float4(0, 0, 0, 0);
-            if (keep) { lo = S.qlo[s]; hi = S.qhi[s]; }
+            if (keep) { lo = qlo[s]; hi = qhi[s]; }
             __syncwarp();
             if (keep) {
                 int dst = base + __popc(km & lanemask_lt());
-                S.qlo[dst] = lo;
-                S.qhi[dst] = hi;
+                qlo[dst] = lo;
+                qhi[dst] = hi;
             }
             __syncwarp();
             base += __popc(km);
@@ -1078,6 +1171,10 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
     c.nv = 8;
     c.np = 6;
     c.nq = 0;
+    if (T::SPHERE) {
+        c.flo[0] = c.flo[1] = c.flo[2] = 0.f;
+        c.fhi[0] = c.fhi[1] = c.fhi[2] = 0.f;
+    }
     __syncwarp();
     update_aabb(S, c, lane);
 }
@@ -1141,20 +1238,31 @@ __device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int
         const float4 sj = J.sj;
         const double tol = J.tol;
         const int nch = (nv + 31) >> 5;
-        for (int ch = w; ch < nch; ch += T::WARPS) {
-            const int s = ch * 32 + lane;
-            bool out = false;
-            if (s < nv) {
-                float4 v = S.fv[s];
-                float s32 = fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d;
-                if (fabsf(s32) > f.m) out = s32 > 0.f;
-                else {
-                    const double4 pe = exact_plane(c, sj);
-                    out = fma(pe.x, S.vx[s], fma(pe.y, S.vy[s], pe.z * S.vz[s])) - pe.w > tol;
-                }
+        constexpr int U = 4;  // chunks in flight per warp (the vertex loads are independent)
+        for (int ch0 = w; ch0 < nch; ch0 += U * T::WARPS) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int s = (ch0 + u * T::WARPS) * 32 + lane;
+                v[u] = s < nv ? S.fv[s] : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            const unsigned m = __ballot_sync(FULL, out);
-            if (lane == 0) S.omask[ch] = m;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int ch = ch0 + u * T::WARPS;
+                if (ch >= nch) break;
+                const int s = ch * 32 + lane;
+                bool out = false;
+                if (s < nv) {
+                    float s32 = fmaf(f.nx, v[u].x, fmaf(f.ny, v[u].y, f.nz * v[u].z)) - f.d;
+                    if (fabsf(s32) > f.m) out = s32 > 0.f;
+                    else {
+                        const double4 pe = exact_plane(c, sj);
+                        out = fma(pe.x, S.vx[s], fma(pe.y, S.vy[s], pe.z * S.vz[s])) - pe.w > tol;
+                    }
+                }
+                const unsigned m = __ballot_sync(FULL, out);
+                if (lane == 0) S.omask[ch] = m;
+            }
         }
     } else if (kind == JOB_EXACT) {
         const unsigned mask = J.mask;
@@ -1167,7 +1275,19 @@ __device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int
     } else if (kind == JOB_AABB) {
         Box6 b;
         b.reset();
-        for (int s = w * 32 + lane; s < nv; s += stride) b.add(S.fv[s]);
+        const float4 m = J.lo[0];
+        float sr2 = 0.f;
+#pragma unroll 4
+        for (int s = w * 32 + lane; s < nv; s += stride) {
+            const float4 v = S.fv[s];
+            b.add(v);
+            if (T::SPHERE) {
+                const float dx = v.x - m.x, dy = v.y - m.y, dz = v.z - m.z;
+                sr2 = fmaxf(sr2, dx * dx + dy * dy + dz * dz);
+            }
+        }
+        const int r6 = __reduce_max_sync(FULL, ford(sr2));
+        if (lane == 0) J.ipart[w][6] = r6;
         int r0 = __reduce_min_sync(FULL, ford(b.lo0)), r1 = __reduce_min_sync(FULL, ford(b.lo1)),
             r2 = __reduce_min_sync(FULL, ford(b.lo2)), r3 = __reduce_max_sync(FULL, ford(b.hi0)),
             r4 = __reduce_max_sync(FULL, ford(b.hi1)), r5 = __reduce_max_sync(FULL, ford(b.hi2));
@@ -1175,6 +1295,65 @@ __device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int
             J.ipart[w][0] = r0; J.ipart[w][1] = r1; J.ipart[w][2] = r2;
             J.ipart[w][3] = r3; J.ipart[w][4] = r4; J.ipart[w][5] = r5;
         }
+    } else if (kind == JOB_BATCH) {
+        // does candidate k's plane cut the cell?  cut: some vertex certainly outside; amb: some vertex
+        // within the FP32 margin (the caller certifies those in FP64)
+        const unsigned cmask = J.mask;
+        unsigned cut = 0u, amb = 0u;
+        constexpr int U = 4;
+        for (int s0 = w * 32 + lane; s0 < nv; s0 += U * stride) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int sv = s0 + u * stride;
+                v[u] = sv < nv ? S.fv[sv] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            unsigned mm = cmask;
+            while (mm) {
+                const int k = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const float4 D = J.cD[k];
+                const float mk = J.cm[k];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (s0 + u * stride < nv) {
+                        const float sv = fmaf(D.x, v[u].x, fmaf(D.y, v[u].y, D.z * v[u].z)) - D.w;
+                        if (sv > mk) cut |= 1u << k;
+                        else if (fabsf(sv) <= mk) amb |= 1u << k;
+                    }
+                }
+            }
+        }
+        cut = __reduce_or_sync(FULL, cut);
+        amb = __reduce_or_sync(FULL, amb);
+        if (lane == 0) { J.ipart[w][0] = (int)cut; J.ipart[w][1] = (int)amb; }
+    } else if (kind == JOB_REVAL) {
+        // re-validate the queue against the shrunk cell: alive ballots per chunk + this warp's best
+        const int nq = J.nq;
+        const unsigned flags = J.flags;
+        float4* const qlo = coop_queue_lo<T>();
+        float4* const qhi = coop_queue_hi<T>();
+        uint32_t* const qmask = coop_queue_mask<T>();
+        const int qch = (nq + 31) >> 5;
+        int bestk = 0x7fffffff, bests = 0x7fffffff;
+        for (int ch = w; ch < qch; ch += T::WARPS) {
+            const int sq = ch * 32 + lane;
+            bool al = false;
+            if (sq < nq) {
+                bool culled;
+                const float k = node_test(c, qlo[sq], qhi[sq], flags, culled);
+                al = !culled;
+                if (al && ford(k) < bestk) { bestk = ford(k); bests = sq; }
+            }
+            const unsigned am = __ballot_sync(FULL, al);
+            if (lane == 0) qmask[ch] = am;
+        }
+        const int gk = __reduce_min_sync(FULL, bestk);
+        const int gs = __reduce_min_sync(FULL, bestk == gk ? bests : 0x7fffffff);
+        int alive = 0;
+        for (int ch = w + lane * T::WARPS; ch < qch; ch += 32 * T::WARPS) alive += __popc(qmask[ch]);
+        alive = __reduce_add_sync(FULL, alive);
+        if (lane == 0) { J.ipart[w][0] = gk; J.ipart[w][1] = gs; J.ipart[w][2] = alive; }
     } else if (kind == JOB_TWINS) {
         twins_range(S, nv, w * 32 + lane, stride);
     } else if (kind == JOB_AREAS) {
@@ -1198,6 +1377,50 @@ __device__ __noinline__ void coop_worker(WarpState<T>& S, int w, int lane) {
     }
 }
 
+// Dual tetrahedra (PD_TETS): vertex (a, b, c) of cell i whose three planes are bisector faces of
+// positive area is the power-equidistant centre of {i, j_a, j_b, j_c}; the tet is written by the cell
+// of its lowest original id, as (i, sorted others).  Needs S.farea (finalize).
+template <class T>
+__device__ __noinline__ void emit_tets(WarpState<T>& S, const Cell& c, int lane, const CellParams& P, double amin) {
+    const CellOut& O = P.out;
+    const int i = c.self_orig;
+    int total = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        long long base = 0;
+        if (pass == 1) {
+            if (lane == 0) base = (long long)atom_add_g(O.ttop, (unsigned long long)total);
+            base = __shfl_sync(FULL, base, 0);
+            if (base + total > O.tcap) {  // arena full: the build is re-run with a larger one
+                if (lane == 0) { *O.tovf = 1; O.tcnt[i] = 0; O.taoff[i] = 0; }
+                break;
+            }
+            if (lane == 0) { O.tcnt[i] = total; O.taoff[i] = base; }
+        }
+        int k = 0;
+        for (int u0 = 0; u0 < c.nv; u0 += 32) {
+            const int u = u0 + lane;
+            bool em = false;
+            int x = 0, y = 0, z = 0;
+            if (u < c.nv) {
+                const auto t = S.vt[u];
+                const int a = ta(t), b = tb(t), cc = tc(t);
+                const int pa = S.pid[a], pb = S.pid[b], pc = S.pid[cc];
+                if (pa >= 0 && pb >= 0 && pc >= 0 && S.farea[a] > amin && S.farea[b] > amin && S.farea[cc] > amin) {
+                    x = __ldg(&P.perm[pa]); y = __ldg(&P.perm[pb]); z = __ldg(&P.perm[pc]);
+                    if (x > y) { int q = x; x = y; y = q; }
+                    if (y > z) { int q = y; y = z; z = q; }
+                    if (x > y) { int q = x; x = y; y = q; }
+                    em = i < x;
+                }
+            }
+            const unsigned m = __ballot_sync(FULL, em);
+            if (pass == 1 && em) O.tarena[base + k + __popc(m & lanemask_lt())] = make_int4(i, x, y, z);
+            k += __popc(m);
+        }
+        total = k;
+    }
+}
+
 // Face areas (vector area 1/2 sum v x next(v) around each face), volume, neighbours; FP64.
 template <class T>
 __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const CellParams& P, int status) {
@@ -1205,6 +1428,7 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
     const CellOut& O = P.out;
     if (status == ST_EMPTY || status == ST_DUP || status == ST_OVERFLOW) {
         if (lane == 0) {
+            if (O.tarena) { O.tcnt[i] = 0; O.taoff[i] = 0; }
             O.cnt[i] = 0;
             O.aoff[i] = 0;
             O.vol[i] = 0.f;
@@ -1274,6 +1498,7 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
     } else if (lane == 0) {
         *O.arena_overflow = 1;
     }
+    if (O.tarena) emit_tets(S, c, lane, P, amin);
     if (lane == 0) {
         O.cnt[i] = K;
         O.aoff[i] = base;
@@ -1337,7 +1562,9 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             c.px = site.x; c.py = site.y; c.pz = site.z; c.pw = site.w;
             c.self = s;
             c.self_orig = __ldg(&P.perm[s]);
+#if PD_PROFILE
             const long long t_cell = clock64();
+#endif
             PT_BEGIN(t_init);
             init_cell(S, c, lane, P);
             PT_END(t_init, 0);
@@ -1358,7 +1585,9 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             finalize(S, c, lane, P, st);
             PT_END(t_fin, 5);
             ncells++;
+#if PD_PROFILE
             if (c.self_orig == P.trace_cell && lane == 0) trace_print(tier, c, cnt, before, st, clock64() - t_cell);
+#endif
             if ((P.flags & PD_COST) && lane == 0) {  // deterministic work count (balanced cuts must agree)
                 unsigned long long w = (cnt.nodes - before.nodes) + (cnt.sites - before.sites) + 8 * (cnt.clips - before.clips);
                 P.out.cost[c.self_orig] = (int32_t)min(w, 0x7fffffffull);
@@ -1389,7 +1618,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
 template <class T, unsigned MODE>
 int tier_grid(int num_sms) {
     if (T::GLOBAL) {
-        if (T::COOP) cudaFuncSetAttribute(cells_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CoopJob));
+        if (T::COOP) cudaFuncSetAttribute(cells_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem_bytes<T>());
         return num_sms * kTier3BlocksPerSM;
     }
     size_t smem = sizeof(WarpState<T>) * T::WARPS;
@@ -1402,7 +1631,7 @@ int tier_grid(int num_sms) {
 
 template <class T, unsigned MODE>
 cudaError_t launch_tier(const CellParams& p, int tier, cudaStream_t st, int num_sms) {
-    size_t smem = T::COOP ? sizeof(CoopJob) : T::GLOBAL ? 0 : sizeof(WarpState<T>) * T::WARPS;
+    size_t smem = T::COOP ? coop_smem_bytes<T>() : T::GLOBAL ? 0 : sizeof(WarpState<T>) * T::WARPS;
     int grid = tier_grid<T, MODE>(num_sms);
     cells_kernel<T, MODE><<<grid, T::WARPS * 32, smem, st>>>(p, tier);
     return cudaGetLastError();

@@ -84,6 +84,17 @@ __global__ void k_assemble_rows(const int32_t* __restrict__ perm, int64_t n, con
     }
 }
 
+// dual tetrahedra: one thread per cell copies its rows (int4 each)
+__global__ void k_tet_gather(const int32_t* __restrict__ tcnt, const int64_t* __restrict__ taoff,
+                             const int64_t* __restrict__ toff, const int4* __restrict__ tarena, int64_t n,
+                             int4* __restrict__ tets) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int c = tcnt[i];
+    const int64_t s = taoff[i], d = toff[i];
+    for (int e = 0; e < c; ++e) tets[d + e] = tarena[s + e];
+}
+
 __global__ void k_fill_u8(uint8_t* p, int64_t n, uint8_t v) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k < n) p[k] = v;
@@ -141,6 +152,13 @@ cudaError_t assemble_rows(const int32_t* perm, int64_t n, const int32_t* cnt_m, 
                           const int64_t* offsets, const int32_t* rows_nbr, const float* rows_area, int32_t* nbr,
                           float* area, cudaStream_t st, int* launches) {
     k_assemble_rows<<<blocks(n, 256), 256, 0, st>>>(perm, n, cnt_m, moff, offsets, rows_nbr, rows_area, nbr, area);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t tet_gather(const int32_t* tcnt, const int64_t* taoff, const int64_t* toff, const int4* tarena, int64_t n,
+                       int4* tets, cudaStream_t st, int* launches) {
+    k_tet_gather<<<blocks(n, 256), 256, 0, st>>>(tcnt, taoff, toff, tarena, n, tets);
     ++*launches;
     return cudaGetLastError();
 }

@@ -47,6 +47,13 @@ struct CellOut {
     int64_t arena_cap;
     int* arena_overflow;            // set to 1 when a row did not fit
     int32_t* cost;                  // optional per-cell work (PD_COST)
+    // optional dual tetrahedra (PD_TETS): per original id count + arena offset, arena of int4 tets
+    int32_t* tcnt;
+    int64_t* taoff;
+    int4* tarena;
+    unsigned long long* ttop;
+    int64_t tcap;
+    int* tovf;
 };
 
 struct Stats {  // device counters (PD_STATS)

@@ -141,9 +141,31 @@ def test_top_tier_cooperative(cfg, n, flags, monkeypatch):
     ref = _gpu(wl, flags=flags)
     monkeypatch.setenv("PD_START_TIER", "2")
     monkeypatch.setenv("PD_COOP_MIN_V", "0")
-    g, o, rep = _assert_parity(wl, flags=flags | pd.STATS)
+    g, o, rep = _assert_parity(wl, flags=flags | pd.STATS | pd.TETS)
     assert np.array_equal(ref.offsets, g.offsets) and np.array_equal(ref.neighbors, g.neighbors)
+    rt = _gpu(wl, flags=flags | pd.TETS).tets
+    assert {tuple(t) for t in np.asarray(g.tets).tolist()} == {tuple(t) for t in np.asarray(rt).tolist()}
     assert np.allclose(ref.volumes, g.volumes, rtol=1e-6)
+
+
+@pytest.mark.parametrize("cfg,n", [("C1", None), ("C2", 4001), ("C3", 4001), ("C5", 4001)])
+def test_dual_tets_parity(cfg, n):
+    """Dual tetrahedra (PD_TETS) equal the oracle's, as sets of sorted id
+    quadruples; host output identical; each tet listed once, grouped by its lowest id."""
+    wl = pdgen.make(cfg, n=n)
+    g = _gpu(wl, flags=pd.TETS)
+    ref, ndeg = oracle.dual_tets(wl.points, wl.weights, wl.box)
+    got = np.asarray(g.tets, np.int64)
+    print(cfg, "tets", len(got), "oracle", len(ref), "degenerate vertices", ndeg)
+    assert np.all(got[:, 0] < got[:, 1]) and np.all(got[:, 1] < got[:, 2]) and np.all(got[:, 2] < got[:, 3])
+    assert np.all(np.diff(got[:, 0]) >= 0)
+    assert len({tuple(t) for t in got.tolist()}) == len(got)
+    assert {tuple(t) for t in got.tolist()} == {tuple(t) for t in ref.tolist()}
+    h = pd.build_diagram(wl.points, wl.weights, wl.box, out_host=True, flags=pd.TETS)
+    assert np.array_equal(h.tets, g.tets)
+    # the diagram itself is unchanged by the extra output
+    ref_d = _gpu(wl)
+    assert np.array_equal(ref_d.offsets, g.offsets) and np.array_equal(ref_d.neighbors, g.neighbors)
 
 
 def test_determinism_bitwise():
@@ -235,6 +257,9 @@ def test_error_contract():
     with pytest.raises(pd.PdError) as e:
         pd.build_diagram(np.zeros((0, 3), np.float32), None, box)
     assert e.value.status == pd.PD_EEMPTY
+    with pytest.raises(pd.PdError) as e:  # dual tets are not available from a sharded build
+        pd.build_diagram(pts, None, box, flags=pd.TETS, shard_rank=0, shard_world=2)
+    assert e.value.status == pd.PD_EINVAL
 
 
 def test_sharded_reassembly_matches_single():

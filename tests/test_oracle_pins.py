@@ -301,3 +301,59 @@ def test_poisson_voronoi_mean_faces():
     deg = np.diff(r.offsets)[inner]
     assert inner.sum() > 8000
     assert abs(deg.mean() - GOLD["poisson_voronoi"]["mean_faces"]) < 0.15
+
+
+# ----------------------------------------------------------------------------- dual tetrahedra
+
+def _center(p, w):
+    """Power centre of 4 sites: |c-p_k|^2 - w_k equal for all k (circumcentre when w = 0)."""
+    A = 2.0 * (p[1:] - p[0])
+    b = np.sum(p[1:] ** 2, axis=1) - np.sum(p[0] ** 2) - (w[1:] - w[0])
+    return np.linalg.solve(A, b)
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_dual_tets_vs_qhull(weighted):
+    """oracle.dual_tets against the library triangulation: scipy Delaunay (unweighted) or the lower
+    hull of the lifted points (weighted, the reduction of PAPER.md:122-123).  Every oracle tet is a
+    triangulation tet, and every triangulation tet whose (power) centre lies inside the box, away
+    from its walls, is an oracle tet."""
+    from scipy.spatial import ConvexHull, Delaunay
+    n = 400
+    pts = pdgen.white_noise(n, 31, 0.0, 1.0)
+    box = (0.0, 0.0, 0.0, 1.0, 1.0, 1.0)
+    p64 = pts.astype(np.float64)
+    if weighted:
+        w = pdgen.weights_paper(n, pdgen.median_nn_distance(pts), 31, ratio=10.0)
+        w64 = w.astype(np.float64)
+        c = p64.mean(axis=0)
+        q = p64 - c
+        hull = ConvexHull(np.concatenate([q, (np.sum(q * q, axis=1) - w64)[:, None]], axis=1))
+        simp = hull.simplices[hull.equations[:, 3] < 0]
+    else:
+        w, w64 = None, np.zeros(n)
+        simp = Delaunay(p64).simplices
+    ref = {tuple(sorted(int(x) for x in s)) for s in simp}
+    got, ndeg = oracle.dual_tets(pts, w, box)
+    assert ndeg == 0 and len(got) > n
+    gset = {tuple(int(x) for x in t) for t in got}
+    assert gset <= ref
+    inside = 0
+    for s in ref:
+        ctr = _center(p64[list(s)], w64[list(s)])
+        if np.all(ctr > 1e-6) and np.all(ctr < 1 - 1e-6):
+            inside += 1
+            assert s in gset, s
+    assert inside > n
+
+
+def test_dual_tets_cube_corner_and_two_sites():
+    """Closed forms: 2 sites -> no tet (every vertex touches a wall); 5 sites = 4 around a centre
+    inside a big box -> the centre's 4 tets {0, a, b, c} of the convex position."""
+    box = (-10.0, -10.0, -10.0, 10.0, 10.0, 10.0)
+    t, _ = oracle.dual_tets(np.array([[0, 0, 0], [1, 0, 0]], np.float32), None, box)
+    assert len(t) == 0
+    P = np.array([[0, 0, 0], [1, 0.1, -0.2], [-0.3, 1, 0.15], [0.2, -0.4, 1.1], [-0.9, -0.8, -0.7]], np.float32)
+    t, _ = oracle.dual_tets(P, None, box)
+    # the centre site 0 lies inside the tetrahedron of the other four: Delaunay = 4 tets around it
+    assert sorted(map(tuple, t.tolist())) == [(0, 1, 2, 3), (0, 1, 2, 4), (0, 1, 3, 4), (0, 2, 3, 4)]
