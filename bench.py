@@ -181,7 +181,7 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
-    base_flags = pd.WARM_START if args.warm_start else 0
+    base_flags = pd.WARM_START if args.warm_start else (pd.WARM_ADAPTIVE if args.warm_adaptive else 0)
 
     def step(flags=0):
         flags |= base_flags
@@ -269,7 +269,7 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
                 "config": {"workload": f"{wl.name}: {wl.description}", "n": wl.n, "box": list(wl.box),
                            "leaf_size": args.leaf or 32, "parallelism": f"seed-sharded x{world}",
-                           "warm_start": bool(args.warm_start),
+                           "warm_start": "all" if args.warm_start else ("adaptive" if args.warm_adaptive else "off"),
                            "l2": "flushed before every timed step (256 MiB write)", "generation_s": round(gen_s, 1)},
                 "roofline": roof,
                 "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
@@ -299,7 +299,8 @@ def main():
     ap.add_argument("--leaf", type=int, default=0)
     ap.add_argument("--ref-cells", type=int, default=64, help="reference arm: cells per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--warm-start", action="store_true", help="KNN warm start (PAPER.md:544-545)")
+    ap.add_argument("--warm-start", action="store_true", help="KNN warm start of every cell (PAPER.md:544-545)")
+    ap.add_argument("--warm-adaptive", action="store_true", help="KNN warm start of the dominated sites only")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

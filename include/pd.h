@@ -58,15 +58,19 @@ enum {
     PD_STATS = 1u << 2,       /* collect traversal/clipping counters (pd_get_stats) */
     PD_ISOTROPIC = 1u << 3,   /* ablation: isotropic radius instead of the directional one */
     PD_DFS = 1u << 4,         /* ablation: depth-first LIFO traversal instead of best-first */
-    PD_WARM_START = 1u << 5,  /* KNN warm start (K = 8): a K-nearest-neighbour query on the
-                                 same BVH pre-clips every cell before its traversal; same diagram, different
-                                 work (the neighbour sets are identical, areas/volumes agree to rounding) */
+    PD_WARM_START = 1u << 5,  /* KNN warm start (K = 8): a K-nearest-neighbour query (in power
+                                 distance pi_j(p_i) = |p_i-p_j|^2 - w_j) on the same BVH pre-clips every cell
+                                 before its traversal; same diagram, different work (the neighbour sets are
+                                 identical, areas/volumes agree to rounding) */
     PD_PAPER_BOUND = 1u << 6, /* ablation: the paper's culling bounds only (no AABB-support companion) */
     PD_COST = 1u << 7,        /* record per-cell work (pd_cell_cost): BVH nodes + leaf sites + 8 x clips (deterministic) */
     PD_EXACT_NODES = 1u << 8, /* exact polytope-vs-box node test on every node the AABB tests keep */
     PD_NO_EXACT = 1u << 9,    /* never use the exact polytope-vs-box node test (pure AABB culling) */
     PD_BALANCE = 1u << 10,    /* sharded build: equal-cost Morton slices from a sampled cost estimate
                                  (default: equal-count slices, measured better balanced on C4) */
+    PD_WARM_ADAPTIVE = 1u << 12, /* warm start only the sites whose power-nearest neighbour dominates them at
+                                    their own position (every EMPTY cell is such a site): the KNN query runs for
+                                    all, the pre-clip only where it pays (heavy-tailed weights) */
     PD_TETS = 1u << 11        /* also output the dual tetrahedra (the "explicit mesh"
                                  of PAPER.md:343/398): see pd_tets.  Not with shard_world > 1 (PD_EINVAL). */
 };

@@ -423,12 +423,13 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         // ---- optional KNN warm start: K = 8 nearest sites of every site of the slice
         int32_t* knn = nullptr;
         cudaEvent_t kev[2] = {nullptr, nullptr};
-        if (opt.flags & PD_WARM_START) {
+        if (opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE)) {
             knn = W.alloc<int32_t>((size_t)n * pd::KNN_K);
             ck(cudaEventCreate(&kev[0]));
             ck(cudaEventCreate(&kev[1]));
             ck(cudaEventRecord(kev[0], st));
-            ck(pd::knn_query(sorted, bvh.nodes, bvh.root, (int)begin, (int)end, knn, sms, st, &launches));
+            const int adaptive = (opt.flags & PD_WARM_START) ? 0 : 1;
+            ck(pd::knn_query(sorted, bvh.nodes, bvh.root, (int)begin, (int)end, adaptive, knn, sms, st, &launches));
             ck(cudaEventRecord(kev[1], st));
         }
         int32_t* lists = W.alloc<int32_t>(2 * (size_t)std::max<int64_t>(end - begin, 1));
@@ -479,6 +480,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.root = bvh.root;
             for (int k = 0; k < 3; ++k) { P.box_lo[k] = hbox[k]; P.box_hi[k] = hbox[3 + k]; }
             P.flags = opt.flags;
+            if (opt.flags & PD_WARM_ADAPTIVE) P.flags = (P.flags & ~PD_WARM_ADAPTIVE) | PD_WARM_START;
             P.out.cnt = cnt;
             P.out.aoff = aoff;
             P.out.vol = vol;
@@ -504,6 +506,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.exact_after = exact_after;
             P.prof_tier = getenv("PD_PROF_TIER") ? atoi(getenv("PD_PROF_TIER")) : -1;
             P.knn = knn;
+            P.n_sites = n;
             P.start_tier = getenv("PD_START_TIER") ? atoi(getenv("PD_START_TIER")) : 0;
             P.coop_min_v = getenv("PD_COOP_MIN_V") ? atoi(getenv("PD_COOP_MIN_V")) : 128;
             P.trace_cell = getenv("PD_TRACE_CELL") ? atoi(getenv("PD_TRACE_CELL")) : -1;

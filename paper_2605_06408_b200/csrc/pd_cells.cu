@@ -897,20 +897,39 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
     return ST_OK;
 }
 
+// A BVH leaf's sites -- or, once per cell with the KNN warm start, the site's K
+// power-nearest sites, clipped before the traversal through this same (single, inlined) candidate
+// path.  The warm-start sites are met again in their leaves, where their planes no longer cut
+// (on-plane vertices are kept), so the diagram is unchanged.  Coincident sites
+// are never in the list; they share a Morton code, so they sit next to each other in Morton order, and
+// the duplicate rule (R5) is settled from the 16 positions on either side before any warm-start clip
+// (so a cell that the power-nearest planes empty is still flagged DUPLICATE when it is one; the leaf
+// processing keeps deciding the rare runs of > 16 sites in one Morton cell).
 template <class T, unsigned MODE>
-__device__ __forceinline__ int process_leaf(WarpState<T>& S, Cell& c, int lane, int link, const CellParams& P, Counters& cnt) {
-    const int first = leaf_first(link), count = leaf_count(link);
-    const int j = first + lane;
-    return process_cands<T, MODE>(S, c, lane, j, lane < count && j != c.self, count, P, cnt);
-}
-
-// KNN warm start: clip by the site's K nearest sites before the traversal.  Those
-// sites are met again in their leaves, where their planes no longer cut (on-plane vertices are kept,
-// SURVEY.md §8(c) Q11), so the diagram is unchanged; coincident sites are never in the list.
-template <class T, unsigned MODE>
-__device__ __noinline__ int warm_start(WarpState<T>& S, Cell& c, int lane, const CellParams& P, Counters& cnt) {
-    const int j = lane < KNN_K ? __ldg(&P.knn[(int64_t)c.self * KNN_K + lane]) : -1;
-    return process_cands<T, MODE>(S, c, lane, j, j >= 0, KNN_K, P, cnt);
+__device__ __forceinline__ int process_leaf(WarpState<T>& S, Cell& c, int lane, int link, bool warm, const CellParams& P,
+                                            Counters& cnt) {
+    int j, count;
+    bool valid;
+    if ((mode_flags<MODE>(P.flags) & PD_WARM_START) && warm) {
+        j = lane < KNN_K ? __ldg(&P.knn[(int64_t)c.self * KNN_K + lane]) : -1;
+        if (!__any_sync(FULL, j >= 0)) return ST_OK;  // no list (adaptive mode: not dominated)
+        const int64_t t = lane < 16 ? (int64_t)c.self - 1 - lane : (int64_t)c.self + 1 + (lane - 16);
+        bool kill = false;
+        if (t >= 0 && t < P.n_sites) {
+            const float4 q = __ldg(&P.sites[t]);
+            if (q.x == c.fpx && q.y == c.fpy && q.z == c.fpz)
+                kill = q.w > c.fpw || (q.w == c.fpw && __ldg(&P.perm[t]) < c.self_orig);
+        }
+        if (__any_sync(FULL, kill)) return ST_DUP;
+        valid = j >= 0;
+        count = KNN_K;
+    } else {
+        const int first = leaf_first(link);
+        count = leaf_count(link);
+        j = first + lane;
+        valid = lane < count && j != c.self;
+    }
+    return process_cands<T, MODE>(S, c, lane, j, valid, count, P, cnt);
 }
 
 // Best-first traversal (Alg. 1).  Queue entries are the pushed child records;
@@ -927,13 +946,16 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
     uint32_t* const qmask = T::COOP ? coop_queue_mask<T>() : S.qmask;
     int node = __float_as_int(__ldg(&P.root->hi_l.w));
     bool have = true;
+    // warm start: the first "leaf" is the KNN list (then the traversal starts at the root)
+    bool warm = (mode_flags<MODE>(P.flags) & PD_WARM_START) && P.knn;
+    const int root_link = node;
     int ns = 0;  // spilled entries
     const unsigned long long nodes0 = cnt.nodes;
     int nq = 0;  // queue length (warp-uniform register)
     for (;;) {
         if (have) {
             PT_BEGIN(t_desc);
-            while (node >= 0) {  // descend (Alg. 1 lines 4-18), 8 children per visit
+            while (node >= 0 && !warm) {  // descend (Alg. 1 lines 4-18), 8 children per visit
                 cnt.nodes++;
                 float key = INFINITY;
                 bool culled = true;
@@ -1011,9 +1033,14 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 cnt.leaves++;
                 __syncwarp();
                 PT_BEGIN(t_leaf);
-                int st = process_leaf<T, MODE>(S, c, lane, node, P, cnt);
+                int st = process_leaf<T, MODE>(S, c, lane, node, warm, P, cnt);
                 PT_END(t_leaf, 2);
                 if (st != ST_OK) return st;
+                if (warm) {
+                    warm = false;
+                    node = root_link;
+                    continue;
+                }
             }
         }
         // pop (Alg. 1 lines 21-31): re-validate every queued entry against the shrunk cell
@@ -1578,10 +1605,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             PT_BEGIN(t_init);
             init_cell(S, c, lane, P);
             PT_END(t_init, 0);
-            int st = ST_OK;
-            if ((mode_flags<MODE>(P.flags) & PD_WARM_START) && P.knn) st = warm_start<T, MODE>(S, c, lane, P, cnt);
-            __syncwarp();
-            if (st == ST_OK) st = traverse<T, MODE>(S, c, lane, P, cnt, spill, P.spill_cap);
+            int st = traverse<T, MODE>(S, c, lane, P, cnt, spill, P.spill_cap);
             __syncwarp();
             if (st == ST_OVERFLOW && !P.last_tier) {
                 if (lane == 0) {

@@ -85,6 +85,7 @@ struct CellParams {
     void* gstate;       // top tier: per-warp cell state in global memory
     int prof_tier;      // PD_PROFILE builds: tier whose phase cycles are recorded (-1 = all)
     const int32_t* knn; // PD_WARM_START: K = 8 nearest sites per Morton index (-1 = none), else NULL
+    int64_t n_sites;    // number of sites (Morton positions 0..n_sites-1)
     int start_tier;     // test knob ($PD_START_TIER): cells skip the tiers below it (default 0)
     int coop_min_v;     // top tier: vertex count from which O(V) passes use the whole CTA ($PD_COOP_MIN_V)
     int trace_cell;     // debug ($PD_TRACE_CELL): print the work counters of this original id (-1 = none)
@@ -95,7 +96,8 @@ int cells_grid_warps(int tier, int num_sms);
 size_t cells_global_state_bytes(int num_sms);
 constexpr int KNN_K = 8;  // warm-start neighbours per site
 // K nearest sites (Euclidean, coincident sites excluded) of the Morton positions [begin, end) -> knn[s*K + k]
-cudaError_t knn_query(const float4* sites, const WideNode* nodes, const NodeChild* root, int begin, int end, int32_t* knn,
-                      int num_sms, cudaStream_t st, int* launches);
+// adaptive != 0: only sites dominated at their own position by their power-nearest neighbour keep a list
+cudaError_t knn_query(const float4* sites, const WideNode* nodes, const NodeChild* root, int begin, int end, int adaptive,
+                      int32_t* knn, int num_sms, cudaStream_t st, int* launches);
 
 }  // namespace pd

@@ -3,8 +3,13 @@
 // BVH gives each site candidates that pre-clip its cell, so the directional culling
 // already prunes from the root.
 //
+// "Nearest" is in power distance from the site, pi_j(p_i) = |p_i - p_j|^2 - w_j (PAPER.md:545 bounds the
+// initial search radius "to approximately the power distance to the K-th nearest neighbor"; for
+// Voronoi input it is the Euclidean KNN): the sites whose power cells reach furthest over p_i, which
+// for a light site among heavy ones are the planes that empty its cell.
 // One warp per site over the 8-wide BVH: lanes 0..7 test the 8 child boxes of a node (squared
-// distance from the site to the box), the nearest surviving child is descended, the others go on a
+// distance from the site to the box minus the subtree's max weight, a lower bound of the power
+// distance), the nearest surviving child is descended, the others go on a
 // per-warp stack in shared memory (popped nearest-last-pushed, re-checked against the current K-th
 // distance); at a leaf lane k takes site first+k and the candidates closer than the current K-th are
 // inserted one at a time into the sorted best list held by lanes 0..7.
@@ -32,7 +37,8 @@ __device__ __forceinline__ int fordk(float f) {
 }
 
 __global__ void __launch_bounds__(KNN_WARPS * 32) k_knn(const float4* __restrict__ sites, const WideNode* __restrict__ nodes,
-                                                        const NodeChild* __restrict__ root, int begin, int end, int32_t* __restrict__ knn) {
+                                                        const NodeChild* __restrict__ root, int begin, int end, int adaptive,
+                                                        int32_t* __restrict__ knn) {
     __shared__ int st_node[KNN_WARPS][KNN_STACK];
     __shared__ float st_d[KNN_WARPS][KNN_STACK];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -55,11 +61,11 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) k_knn(const float4* __restrict
                         const NodeChild* rec = nodes[node].c;
                         float4 lo = __ldg(&rec[lane].lo_w), hi = __ldg(&rec[lane].hi_l);
                         link = __float_as_int(hi.w);
-                        if (link != EMPTY_LINK) {
+                        if (link != EMPTY_LINK) {  // lower bound of the power distance over the box
                             float gx = fmaxf(fmaxf(lo.x - p.x, p.x - hi.x), 0.f);
                             float gy = fmaxf(fmaxf(lo.y - p.y, p.y - hi.y), 0.f);
                             float gz = fmaxf(fmaxf(lo.z - p.z, p.z - hi.z), 0.f);
-                            d = gx * gx + gy * gy + gz * gz;
+                            d = gx * gx + gy * gy + gz * gz - lo.w;
                         }
                     }
                     const bool ok = d < kth;
@@ -83,7 +89,7 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) k_knn(const float4* __restrict
                 if (lane < count && j != s) {
                     const float4 q = __ldg(&sites[j]);
                     const float dx = q.x - p.x, dy = q.y - p.y, dz = q.z - p.z;
-                    if (dx != 0.f || dy != 0.f || dz != 0.f) d = dx * dx + dy * dy + dz * dz;
+                    if (dx != 0.f || dy != 0.f || dz != 0.f) d = dx * dx + dy * dy + dz * dz - q.w;
                 }
                 unsigned cm = __ballot_sync(FULL, d < kth);
                 while (cm) {  // insert the candidates below the K-th distance, one at a time
@@ -109,19 +115,23 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) k_knn(const float4* __restrict
             __syncwarp();
             if (!have) break;
         }
-        if (lane < KNN_K) knn[(int64_t)s * KNN_K + lane] = bi;
+        // adaptive mode: keep the list only for a site that its power-nearest neighbour dominates at
+        // its own position (pi_j(p_i) < pi_i(p_i) = -w_i: p_i lies outside its cell, as for every EMPTY
+        // cell), where pre-clipping pays; other sites start the traversal from the box as usual
+        const bool keep = !adaptive || __shfl_sync(FULL, bd, 0) < -p.w;
+        if (lane < KNN_K) knn[(int64_t)s * KNN_K + lane] = keep ? bi : -1;
     }
 }
 
 }  // namespace
 
-cudaError_t knn_query(const float4* sites, const WideNode* nodes, const NodeChild* root, int begin, int end, int32_t* knn,
-                      int num_sms, cudaStream_t st, int* launches) {
+cudaError_t knn_query(const float4* sites, const WideNode* nodes, const NodeChild* root, int begin, int end, int adaptive,
+                      int32_t* knn, int num_sms, cudaStream_t st, int* launches) {
     if (end <= begin) return cudaSuccess;
     int grid = num_sms * 16;
     int need = (end - begin + KNN_WARPS - 1) / KNN_WARPS;
     if (grid > need) grid = need;
-    k_knn<<<grid, KNN_WARPS * 32, 0, st>>>(sites, nodes, root, begin, end, knn);
+    k_knn<<<grid, KNN_WARPS * 32, 0, st>>>(sites, nodes, root, begin, end, adaptive, knn);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

@@ -96,7 +96,8 @@ def test_leaf_sizes_identical(leaf):
     assert np.allclose(ref.volumes, g.volumes, rtol=1e-6, atol=0)
 
 
-@pytest.mark.parametrize("flag", [pd.ISOTROPIC, pd.DFS, pd.PAPER_BOUND, pd.WARM_START, pd.WARM_START | pd.DFS])
+@pytest.mark.parametrize("flag", [pd.ISOTROPIC, pd.DFS, pd.PAPER_BOUND, pd.WARM_START, pd.WARM_START | pd.DFS,
+                                  pd.WARM_ADAPTIVE])
 def test_ablations_neutral(flag):
     """Culling / traversal variants change the work, not the diagram."""
     wl = pdgen.make("C3", n=8009)
@@ -112,6 +113,7 @@ def test_warm_start_parity(cfg, n):
     with a leaf of one site (KNN over single-site leaves)."""
     _assert_parity(pdgen.make(cfg, n=n), flags=pd.WARM_START)
     _assert_parity(pdgen.make(cfg, n=n), flags=pd.WARM_START, leaf_size=1)
+    _assert_parity(pdgen.make(cfg, n=n), flags=pd.WARM_ADAPTIVE)
 
 
 def test_warm_start_duplicates_and_lattice():
@@ -123,6 +125,13 @@ def test_warm_start_duplicates_and_lattice():
     b = pd.build_diagram(pts, None, box, out_host=True, flags=pd.WARM_START)
     for k in ("offsets", "neighbors", "flags"):
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
+    # weighted duplicates: the heavy coincident pair must stay EMPTY|DUPLICATE even when a power-nearest
+    # heavy neighbour empties the light one first
+    pts2 = np.array([[0.5, 0.5, 0.5], [0.5, 0.5, 0.5], [0.52, 0.5, 0.5], [0.2, 0.3, 0.4]], np.float32)
+    w2 = np.array([0.0, 0.001, 0.5, 0.0], np.float32)
+    a = pd.build_diagram(pts2, w2, box, out_host=True)
+    b = pd.build_diagram(pts2, w2, box, out_host=True, flags=pd.WARM_START)
+    assert np.array_equal(a.flags, b.flags) and a.flags[0] & pd.CELL_DUPLICATE
     gr = np.arange(-3, 4, dtype=np.float64)
     P = (np.stack(np.meshgrid(gr, gr, gr, indexing="ij"), -1).reshape(-1, 3) * 0.5).astype(np.float32)
     a = pd.build_diagram(P, None, (-1.8,) * 3 + (1.8,) * 3, out_host=True)
