@@ -264,6 +264,11 @@ def run_ours(args):
                 "kernel_ms": kms, "kernel_share_of_step": kms / ms if world == 1 else None,
                 "work_model": "W_min = 2.3e4 FP ops/cell (SURVEY.md §8(d)); peak = 148 SM x 128 lanes x 1.965 GHz "
                               "(derived, not measured; MEASURED_PEAKS.json has no FP32 figure)"}
+        if traffic:  # what actually bounds it (ncu, tier-1 launch on C4): instruction issue, not FP32 or DRAM
+            roof["ncu_issue_slot_util"] = traffic.get("issue_active_pct", 0) / 100.0
+            roof["ncu_warps_active"] = traffic.get("warps_active_pct", 0) / 100.0
+            roof["ncu_dram_gbs"] = traffic["dram_bytes_per_launch"] / traffic["duration_ns"]
+            roof["ncu_warp_inst_per_cell"] = traffic["inst_executed"] / 1e7
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",

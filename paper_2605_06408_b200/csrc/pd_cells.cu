@@ -332,8 +332,9 @@ struct CoopJob {
     double dpart[kCoopMaxW][2];
     unsigned flags;     // JOB_REVAL: culling mode
     int nq;             // JOB_REVAL: queue length
-    float4 cD[32];      // JOB_BATCH: candidate planes (D, d) of a leaf, lane = candidate
-    float cm[32];       //            and their FP32 certification margins
+    float4 cD[32];      // JOB_BATCH: candidate planes (D, d) of a leaf, lane = candidate,
+    float cm[32];       //            their FP32 certification margins
+    float4 csj[32];     //            and sites (for the FP64 certification of ambiguous vertices)
 };
 extern __shared__ __align__(16) unsigned char pd_smem[];
 __device__ __forceinline__ CoopJob& coop_job() { return *reinterpret_cast<CoopJob*>(pd_smem); }
@@ -855,13 +856,12 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         // cooperative tier: one CTA-wide pass tests every candidate of the leaf against the current
         // cell (same certified predicate); only the planes that cut go on to clip()
         CoopJob& J = coop_job();
-        if (cand) { J.cD[lane] = make_float4(Dx, Dy, Dz, dd); J.cm[lane] = m; }
+        if (cand) { J.cD[lane] = make_float4(Dx, Dy, Dz, dd); J.cm[lane] = m; J.csj[lane] = sj; }
         if (lane == 0) { J.kind = JOB_BATCH; J.nv = c.nv; J.mask = mask; }
         coop_go<T>(S, J, lane);
-        unsigned cut = 0u, amb = 0u;
-        for (int w = 0; w < T::WARPS; ++w) { cut |= (unsigned)J.ipart[w][0]; amb |= (unsigned)J.ipart[w][1]; }
-        bool cuts = (cut >> lane) & 1u;
-        if (cand && !cuts && ((amb >> lane) & 1u)) cuts = cuts_fp64(S, c, sj, D2);  // certify in FP64 (rare)
+        unsigned cut = 0u;
+        for (int w = 0; w < T::WARPS; ++w) cut |= (unsigned)J.ipart[w][0];
+        const bool cuts = (cut >> lane) & 1u;
         cnt.tests += __popc(mask);
         cand = cand && cuts;
         mask = __ballot_sync(FULL, cand);
@@ -1333,10 +1333,11 @@ __device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int
             J.ipart[w][3] = r3; J.ipart[w][4] = r4; J.ipart[w][5] = r5;
         }
     } else if (kind == JOB_BATCH) {
-        // does candidate k's plane cut the cell?  cut: some vertex certainly outside; amb: some vertex
-        // within the FP32 margin (the caller certifies those in FP64)
+        // does candidate k's plane cut the cell?  Some vertex outside, by the same certified predicate as
+        // clip(): FP32 beyond the margin, else FP64 against the tolerance 1e-12 |D| R (R9/R10) -- done
+        // right here by the thread holding the vertex (heavy cells' weights make many tests ambiguous)
         const unsigned cmask = J.mask;
-        unsigned cut = 0u, amb = 0u;
+        unsigned cut = 0u;
         constexpr int U = 4;
         for (int s0 = w * 32 + lane; s0 < nv; s0 += U * stride) {
             float4 v[U];
@@ -1353,17 +1354,22 @@ __device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int
                 const float mk = J.cm[k];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    if (s0 + u * stride < nv) {
+                    const int sv_i = s0 + u * stride;
+                    if (sv_i < nv) {
                         const float sv = fmaf(D.x, v[u].x, fmaf(D.y, v[u].y, D.z * v[u].z)) - D.w;
                         if (sv > mk) cut |= 1u << k;
-                        else if (fabsf(sv) <= mk) amb |= 1u << k;
+                        else if (fabsf(sv) <= mk && !((cut >> k) & 1u)) {
+                            const float D2 = fmaf(D.x, D.x, fmaf(D.y, D.y, D.z * D.z));
+                            FPlane f;
+                            f.tl = 1e-12f * (D2 * rsqrtf(D2)) * c.rmax;
+                            if (outside_fp64(c, J.csj[k], f, S.vx[sv_i], S.vy[sv_i], S.vz[sv_i])) cut |= 1u << k;
+                        }
                     }
                 }
             }
         }
         cut = __reduce_or_sync(FULL, cut);
-        amb = __reduce_or_sync(FULL, amb);
-        if (lane == 0) { J.ipart[w][0] = (int)cut; J.ipart[w][1] = (int)amb; }
+        if (lane == 0) { J.ipart[w][0] = (int)cut; J.ipart[w][1] = 0; }
     } else if (kind == JOB_REVAL) {
         // re-validate the queue against the shrunk cell: alive ballots per chunk + this warp's best
         const int nq = J.nq;
