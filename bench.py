@@ -281,7 +281,7 @@ def run_ours(args):
                 "clocks": clocks, "gpu_launches": int(launches),
                 "stats": {k: stats[k] for k in ("nodes_visited", "leaves_visited", "sites_tested", "clip_tests",
                                                  "clips", "tier_cells", "overflow_cells", "ms_bvh", "ms_cells",
-                                                 "ms_csr")},
+                                                 "ms_csr", "ms_tier", "ms_knn")},
                 "nnz": nnz_total, "empty_ratio": float(np.mean(flags_np & 1)),
                 "step_ms": [round(x, 3) for x in step_ms]}
         if world == 1 and not args.no_cpu_baseline:

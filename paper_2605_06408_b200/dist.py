@@ -22,28 +22,37 @@ def exchange_blocks(blocks, group=None):
     """All-gather variable-length Morton-ordered blocks.
 
     blocks = (cnt[int32 L], vol[f32 L], surf[f32 L], flags[u8 L], rows_nbr[int32 T], rows_area[f32 T])
-    for this rank's slice.  Returns the concatenation over ranks in rank order (= Morton order)."""
+    for this rank's slice.  Returns the concatenation over ranks in rank order (= Morton order).
+
+    Three collectives: the (L, T) headers, then the per-cell fields packed as int32 [L, 4]
+    (cnt, vol bits, surf bits, flags) and the rows packed as int32 [T, 2] (id, area bits), each padded
+    to the largest rank's size and gathered into ONE contiguous tensor (all_gather_into_tensor)."""
     world = dist.get_world_size(group)
     cnt, vol, surf, flg, rn, ra = blocks
     dev = cnt.device
     hdr = torch.tensor([cnt.numel(), rn.numel()], dtype=torch.int64, device=dev)
-    hdrs = [torch.empty_like(hdr) for _ in range(world)]
-    dist.all_gather(hdrs, hdr, group=group)
-    sizes = [(int(h[0]), int(h[1])) for h in hdrs]
-    Lmax = max(s[0] for s in sizes)
+    hdrs = torch.empty(world * 2, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(hdrs, hdr, group=group)
+    sizes = hdrs.view(world, 2).tolist()
+    Lmax = max(max(s[0] for s in sizes), 1)
     Tmax = max(max(s[1] for s in sizes), 1)
-
-    def gather(t, n_max, count_of):
-        pad = torch.zeros(n_max, dtype=t.dtype, device=dev)
-        pad[: t.numel()] = t
-        outs = [torch.empty(n_max, dtype=t.dtype, device=dev) for _ in range(world)]
-        dist.all_gather(outs, pad, group=group)
-        return torch.cat([o[: count_of(r)] for r, o in enumerate(outs)])
-
-    cell = lambda r: sizes[r][0]
-    rows = lambda r: sizes[r][1]
-    return (gather(cnt, Lmax, cell), gather(vol, Lmax, cell), gather(surf, Lmax, cell),
-            gather(flg, Lmax, cell), gather(rn, Tmax, rows), gather(ra, Tmax, rows))
+    L, T = cnt.numel(), rn.numel()
+    cells = torch.zeros((Lmax, 4), dtype=torch.int32, device=dev)
+    cells[:L, 0] = cnt
+    cells[:L, 1] = vol.view(torch.int32)
+    cells[:L, 2] = surf.view(torch.int32)
+    cells[:L, 3] = flg.to(torch.int32)
+    rows = torch.zeros((Tmax, 2), dtype=torch.int32, device=dev)
+    rows[:T, 0] = rn
+    rows[:T, 1] = ra.view(torch.int32)
+    cells_all = torch.empty((world * Lmax, 4), dtype=torch.int32, device=dev)
+    rows_all = torch.empty((world * Tmax, 2), dtype=torch.int32, device=dev)
+    dist.all_gather_into_tensor(cells_all, cells, group=group)
+    dist.all_gather_into_tensor(rows_all, rows, group=group)
+    c = torch.cat([cells_all[r * Lmax: r * Lmax + sizes[r][0]] for r in range(world)])
+    w = torch.cat([rows_all[r * Tmax: r * Tmax + sizes[r][1]] for r in range(world)])
+    return (c[:, 0].contiguous(), c[:, 1].contiguous().view(torch.float32), c[:, 2].contiguous().view(torch.float32),
+            c[:, 3].to(torch.uint8), w[:, 0].contiguous(), w[:, 1].contiguous().view(torch.float32))
 
 
 def build_diagram_distributed(points, weights, box, *, group=None, leaf_size: int = 0, flags: int = 0):
