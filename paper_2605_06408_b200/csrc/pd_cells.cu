@@ -104,7 +104,13 @@ struct TierCfg {
 #define PD_T1_SPHERE 0
 #endif
 using Tier1 = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, 4, PD_T1_MINB, false, false, PD_T1_SPHERE != 0>;
-using Tier2 = TierCfg<384, 192, 256, 4, 1, false, false, true>;
+// Tier 2: one cell per CTA of 4 warps (state in shared memory, O(V) passes CTA-wide from 128 vertices):
+// the few heavy cells of a light-weight workload (C4: 78) no longer run on one warp each, which
+// mattered most for the per-rank critical path of sharded builds.
+#ifndef PD_T2_COOP
+#define PD_T2_COOP 0  // measured slower on C3/C4 (the heavy tier-2 cells are traversal-bound), kept as an option
+#endif
+using Tier2 = TierCfg<384, 192, 256, 4, PD_T2_COOP ? 4 : 1, false, PD_T2_COOP != 0, true>;
 // Top tier: state in global memory (L1/L2-cached), 64-bit plane-index triplets; for the rare cells
 // with thousands of faces (heavy-tailed weights, SURVEY.md §7 hard part 3).
 // One cell per CTA: its 16 warps share every O(V) pass (classification, exact node tests, AABB,
@@ -1567,7 +1573,8 @@ __device__ __noinline__ void trace_print(int tier, const Cell& c, const Counters
 template <class T, unsigned MODE>
 __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(CellParams P, int tier) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    WarpState<T>& S = T::COOP     ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x]
+    WarpState<T>& S = T::COOP     ? (T::GLOBAL ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x]
+                                               : *reinterpret_cast<WarpState<T>*>(pd_smem + coop_smem_bytes<T>()))
                       : T::GLOBAL ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x * T::WARPS + wid]
                                   : reinterpret_cast<WarpState<T>*>(pd_smem)[wid];
     if (T::COOP) {
@@ -1585,7 +1592,9 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
     for (int k = lane; k < T::EBW; k += 32) S.ebits[k] = 0u;
     __syncwarp();
     unsigned long long ncells = 0, novf = 0;
-    constexpr int BATCH = 4;
+    // Morton-consecutive batches of 4 in the first tier (locality); one cell at a time from the
+    // (cost-ordered) lists of the higher tiers, so that their heaviest cells spread over the CTAs
+    const int BATCH = P.list ? 1 : 4;
     for (;;) {
         long long b0 = 0;
         if (lane == 0) b0 = (long long)atom_add_g(P.work_counter, (unsigned long long)BATCH);
@@ -1617,6 +1626,11 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
                 if (lane == 0) {
                     int k = atom_add_g32(P.next_count, 1);
                     P.next_list[k] = s;
+                    if (P.next_cost) {  // the host starts the next tier's costliest cells first
+                        unsigned long long w = (cnt.nodes - before.nodes) + (cnt.sites - before.sites) +
+                                               8 * (cnt.clips - before.clips);
+                        P.next_cost[k] = (int32_t)min(w, 0x7fffffffull);
+                    }
                 }
                 continue;
             }
@@ -1661,7 +1675,7 @@ int tier_grid(int num_sms) {
         if (T::COOP) cudaFuncSetAttribute(cells_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)coop_smem_bytes<T>());
         return num_sms * kTier3BlocksPerSM;
     }
-    size_t smem = sizeof(WarpState<T>) * T::WARPS;
+    size_t smem = T::COOP ? coop_smem_bytes<T>() + sizeof(WarpState<T>) : sizeof(WarpState<T>) * T::WARPS;
     cudaFuncSetAttribute(cells_kernel<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cells_kernel<T, MODE>, T::WARPS * 32, smem);
@@ -1671,7 +1685,8 @@ int tier_grid(int num_sms) {
 
 template <class T, unsigned MODE>
 cudaError_t launch_tier(const CellParams& p, int tier, cudaStream_t st, int num_sms) {
-    size_t smem = T::COOP ? coop_smem_bytes<T>() : T::GLOBAL ? 0 : sizeof(WarpState<T>) * T::WARPS;
+    size_t smem = T::COOP ? coop_smem_bytes<T>() + (T::GLOBAL ? 0 : sizeof(WarpState<T>))
+                          : T::GLOBAL ? 0 : sizeof(WarpState<T>) * T::WARPS;
     int grid = tier_grid<T, MODE>(num_sms);
     cells_kernel<T, MODE><<<grid, T::WARPS * 32, smem, st>>>(p, tier);
     return cudaGetLastError();

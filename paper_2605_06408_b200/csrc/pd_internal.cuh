@@ -76,6 +76,7 @@ struct CellParams {
     // overflow hand-off to the next tier
     int32_t* next_list;
     int32_t* next_count;
+    int32_t* next_cost;   // parallel to next_list: the work a cell had done when it outgrew this tier
     int last_tier;
     CellOut out;
     Stats* stats;

@@ -142,13 +142,15 @@ def test_warm_start_duplicates_and_lattice():
 
 @pytest.mark.parametrize("cfg,n", [("C3", 6007), ("C5", 6007)])
 @pytest.mark.parametrize("flags", [0, pd.WARM_START])
-def test_top_tier_cooperative(cfg, n, flags, monkeypatch):
-    """Every cell through the top capacity tier (state in global memory, one cell per CTA) with every
-    O(V) pass CTA-cooperative (classification, exact node tests, AABB, twins, face areas): parity with
-    the oracle and the same neighbour sets as the default tiers."""
+@pytest.mark.parametrize("start_tier", ["1", "2"])
+def test_top_tier_cooperative(cfg, n, flags, start_tier, monkeypatch):
+    """Every cell through a cooperative capacity tier (tier 2: state in shared memory, one cell per CTA
+    of 4 warps; tier 3: state in global memory, one cell per CTA of 16 warps) with every O(V) pass
+    CTA-cooperative (classification, batched cut tests, exact node tests, AABB, queue re-validation,
+    twins, face areas): parity with the oracle and the same neighbour sets as the default tiers."""
     wl = pdgen.make(cfg, n=n)
     ref = _gpu(wl, flags=flags)
-    monkeypatch.setenv("PD_START_TIER", "2")
+    monkeypatch.setenv("PD_START_TIER", start_tier)
     monkeypatch.setenv("PD_COOP_MIN_V", "0")
     g, o, rep = _assert_parity(wl, flags=flags | pd.STATS | pd.TETS)
     assert np.array_equal(ref.offsets, g.offsets) and np.array_equal(ref.neighbors, g.neighbors)
