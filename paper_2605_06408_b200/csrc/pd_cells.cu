@@ -1594,7 +1594,10 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
     unsigned long long ncells = 0, novf = 0;
     // Morton-consecutive batches of 4 in the first tier (locality); one cell at a time from the
     // (cost-ordered) lists of the higher tiers, so that their heaviest cells spread over the CTAs
-    const int BATCH = P.list ? 1 : 4;
+#ifndef PD_T1_BATCH
+#define PD_T1_BATCH 4
+#endif
+    const int BATCH = P.list ? 1 : PD_T1_BATCH;
     for (;;) {
         long long b0 = 0;
         if (lane == 0) b0 = (long long)atom_add_g(P.work_counter, (unsigned long long)BATCH);
