@@ -81,6 +81,10 @@ enum {
     PD_CELL_BOUNDARY = 2,  /* a box wall contributes a face of positive area */
     PD_CELL_OVERFLOW = 4,  /* exceeded the largest on-chip capacity tier: output incomplete */
     PD_CELL_DUPLICATE = 8, /* bit-identical position with a heavier (or equal, lower-id) site */
+    PD_CELL_DEGRADED = 16, /* topology-consistency check failed: a clip's hole boundary
+                              was not one cycle of >= 3 edges, or a face edge of the final cell has no
+                              unique reverse edge; the cell's output is still written, and counted in
+                              pd_stats.degraded_cells */
     PD_CELL_NOT_OWNED = 32 /* sharded build: this cell belongs to another rank's slice */
 };
 
@@ -109,6 +113,12 @@ typedef struct {
     int64_t warp_cycles[10];   /* PD_PROFILE builds only: warp clock64 in init/descend/leaf/clip/pop/finalize,
                                   then clip's classify/boundary/create/aabb */
     double ms_knn;             /* PD_WARM_START: the K-nearest-neighbour query (part of ms_cells) */
+    /* Robustness counters, always collected (BASELINE.json north_star: near-degenerate faces "counted and
+     * reported"; "never silently dropped"): */
+    int64_t faces_dropped;         /* bisector faces with area <= 1e-13 S_i: zero-area contacts, not neighbours
+                                      (reading R2) */
+    int64_t faces_near_degenerate; /* reported neighbour faces with area < 1e-9 S_i (the parity excusal band) */
+    int64_t degraded_cells;        /* cells flagged PD_CELL_DEGRADED */
 } pd_stats;
 
 typedef struct pd_result pd_result;
@@ -157,10 +167,13 @@ int64_t pd_slice_end(const pd_result* r);
 const int32_t* pd_morton_perm(const pd_result* r); /* n; Morton position -> original id (device) */
 
 /* Reassemble a full CSR (original order) from Morton-ordered per-cell blocks gathered from all
- * ranks.  All pointers are DEVICE pointers on opt->device:
+ * ranks.  All pointers are DEVICE pointers on opt->device (rows_nbr/rows_area may be NULL only when
+ * total == 0):
  *   perm[n] (Morton pos -> original id), cnt[n] (row length per Morton pos), vol/surf/flags[n]
  *   per Morton pos, rows_nbr/rows_area[total] concatenated rows in Morton order.
- * Returns a result whose arrays are in original order (on device unless PD_OUT_HOST). */
+ * Returns a result whose arrays are in original order (on device unless PD_OUT_HOST).
+ * Errors: PD_EINVAL if a pointer is NULL, n <= 0, or the row lengths cnt[] do not add up to `total`
+ * (checked on the device before any row is written). */
 pd_status pd_assemble(const int32_t* perm, const int32_t* cnt, const float* vol, const float* surf,
                       const uint8_t* flags, const int32_t* rows_nbr, const float* rows_area,
                       int64_t n, int64_t total, const pd_options* opt, pd_result** out);
@@ -178,6 +191,12 @@ int64_t pd_slice_nnz(const pd_result* r);
  * keys_in/vals_in are not modified; temp storage is allocated internally. */
 pd_status pd_sort_pairs_u64(const uint64_t* keys_in, const uint32_t* vals_in, int64_t n, uint64_t* keys_out,
                             uint32_t* vals_out, void* stream);
+
+/* Release the per-device build workspace (temporaries are cached across builds in persistent device
+ * chunks, DESIGN.md §6 "Memory") and the cached pinned host buffers of freed PD_OUT_HOST results.
+ * Waits for a build in flight on `device`; results stay valid.  Errors: PD_EINVAL (device out of
+ * range), PD_ECUDA. */
+pd_status pd_trim(int device);
 
 const char* pd_strerror(pd_status s);
 int64_t pd_error_index(void);      /* thread-local: offending point of the last NONFINITE/OUTSIDE */

@@ -52,6 +52,8 @@ def lib():
         L.orc_nnz.argtypes = [P]
         L.orc_copy.restype = None
         L.orc_copy.argtypes = [P, P, P, P, P, P, P]
+        L.orc_counts.restype = None
+        L.orc_counts.argtypes = [P, P, P]
         L.orc_free.restype = None
         L.orc_free.argtypes = [P]
         L.orc_cell_geometry.restype = ctypes.c_int
@@ -74,6 +76,8 @@ class OracleCells:
     vol: np.ndarray        # float64 [m]
     surf: np.ndarray       # float64 [m]
     flags: np.ndarray      # uint8 [m]
+    dropped: np.ndarray = None  # int32 [m] bisector faces with area <= 1e-13 S (not neighbours, R2)
+    small: np.ndarray = None    # int32 [m] neighbour faces with area < 1e-9 S (near-degenerate)
 
     def row(self, t):
         a, b = self.offsets[t], self.offsets[t + 1]
@@ -105,9 +109,12 @@ def cells(points, weights, box, ids=None, threads: int | None = None, order_k: i
         surf = np.zeros(m, np.float64)
         flags = np.zeros(m, np.uint8)
         L.orc_copy(r, _ptr(off), _ptr(nbr), _ptr(area), _ptr(vol), _ptr(surf), _ptr(flags))
+        dropped = np.zeros(m, np.int32)
+        small = np.zeros(m, np.int32)
+        L.orc_counts(r, _ptr(dropped), _ptr(small))
     finally:
         L.orc_free(r)
-    return OracleCells(ids, off, nbr[:nnz], area[:nnz], vol, surf, flags)
+    return OracleCells(ids, off, nbr[:nnz], area[:nnz], vol, surf, flags, dropped, small)
 
 
 @dataclass

@@ -235,6 +235,8 @@ typedef struct {
     double vol, surf;
     int flags;
     int32_t* nbr; double* nbr_area; int nnbr;
+    int n_dropped;  /* bisector faces with area <= 1e-13 S (zero-area contacts, not neighbours: R2) */
+    int n_small;    /* neighbour faces with area < 1e-9 S (near-degenerate: BASELINE north_star) */
     /* geometry (optional) */
     poly_t geo;
 } orc_cell;
@@ -342,7 +344,7 @@ static int build_cell(const orc_input* in, int64_t i, orc_ws* ws, int* flags) {
 
 static void finalize_cell(const poly_t* p, orc_cell* out, int flags) {
     out->flags = flags;
-    out->vol = 0; out->surf = 0; out->nnbr = 0; out->nf = 0;
+    out->vol = 0; out->surf = 0; out->nnbr = 0; out->nf = 0; out->n_dropped = 0; out->n_small = 0;
     if (!p) { out->flags |= ORC_EMPTY; return; }
     out->nf = p->nf;
     out->tags = (int*)malloc(sizeof(int) * (p->nf + 1));
@@ -370,7 +372,10 @@ static void finalize_cell(const poly_t* p, orc_cell* out, int flags) {
     for (int f = 0; f < p->nf; ++f) {
         double area = out->areas[f];
         if (out->tags[f] < 0) { if (area > amin) out->flags |= ORC_BOUNDARY; }
-        else if (area > amin) { ta[2 * nt] = (double)out->tags[f]; ta[2 * nt + 1] = area; nt++; }
+        else if (area > amin) {
+            ta[2 * nt] = (double)out->tags[f]; ta[2 * nt + 1] = area; nt++;
+            if (area < 1e-9 * surf) out->n_small++;
+        } else out->n_dropped++;
     }
     qsort(ta, nt, 2 * sizeof(double), tagarea_cmp);
     out->nbr = (int32_t*)malloc(sizeof(int32_t) * (nt + 1));
@@ -463,6 +468,11 @@ void orc_copy(const orc_result* r, int64_t* offsets, int32_t* nbr, double* area,
         vol[t] = c->vol; surf[t] = c->surf; flags[t] = (uint8_t)c->flags;
     }
     offsets[r->ncells] = o;
+}
+
+/* per cell: dropped[t] = bisector faces with area <= 1e-13 S, small[t] = neighbour faces < 1e-9 S */
+void orc_counts(const orc_result* r, int32_t* dropped, int32_t* small) {
+    for (int64_t t = 0; t < r->ncells; ++t) { dropped[t] = r->cells[t].n_dropped; small[t] = r->cells[t].n_small; }
 }
 
 void orc_free(orc_result* r) {

@@ -24,13 +24,13 @@ PD_OK, PD_EINVAL, PD_EEMPTY, PD_ENONFINITE, PD_EOUTSIDE, PD_ENOMEM, PD_ECUDA, PD
 IN_DEVICE, OUT_HOST, STATS, ISOTROPIC, DFS, PAPER_BOUND, COST, EXACT_NODES, NO_EXACT, BALANCE = (
     1, 2, 4, 8, 16, 64, 128, 256, 512, 1024)
 WARM_START, TETS, WARM_ADAPTIVE = 32, 2048, 4096
-CELL_EMPTY, CELL_BOUNDARY, CELL_OVERFLOW, CELL_DUPLICATE, CELL_NOT_OWNED = 1, 2, 4, 8, 32
+CELL_EMPTY, CELL_BOUNDARY, CELL_OVERFLOW, CELL_DUPLICATE, CELL_DEGRADED, CELL_NOT_OWNED = 1, 2, 4, 8, 16, 32
 
 EXPORTED = ["pd_build", "pd_num_cells", "pd_nnz", "pd_on_host", "pd_offsets", "pd_neighbors", "pd_face_areas",
             "pd_volumes", "pd_surface", "pd_cell_flags", "pd_cell_cost", "pd_get_stats", "pd_free", "pd_slice_begin",
             "pd_slice_end", "pd_morton_perm", "pd_assemble", "pd_export_slice", "pd_slice_nnz",
             "pd_strerror", "pd_error_index", "pd_last_cuda_error", "pd_abi_version", "pd_last_launch_count",
-            "pd_sort_pairs_u64", "pd_num_tets", "pd_tets"]
+            "pd_sort_pairs_u64", "pd_num_tets", "pd_tets", "pd_trim"]
 
 
 class PdError(RuntimeError):
@@ -56,7 +56,9 @@ class Stats(ctypes.Structure):
                 ("nnz", ctypes.c_int64),
                 ("ms_bvh", ctypes.c_double), ("ms_cells", ctypes.c_double), ("ms_csr", ctypes.c_double),
                 ("ms_total", ctypes.c_double), ("ms_tier", ctypes.c_double * 3),
-                ("warp_cycles", ctypes.c_int64 * 10), ("ms_knn", ctypes.c_double)]
+                ("warp_cycles", ctypes.c_int64 * 10), ("ms_knn", ctypes.c_double),
+                ("faces_dropped", ctypes.c_int64), ("faces_near_degenerate", ctypes.c_int64),
+                ("degraded_cells", ctypes.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -101,6 +103,8 @@ def load_library(path: str | None = None):
     L.pd_last_cuda_error.restype = ctypes.c_char_p
     L.pd_abi_version.restype = ctypes.c_int
     L.pd_last_launch_count.restype = I64
+    L.pd_trim.restype = ctypes.c_int
+    L.pd_trim.argtypes = [ctypes.c_int]
     if hasattr(L, "pd_tets"):
         L.pd_num_tets.restype = I64
         L.pd_num_tets.argtypes = [P]
@@ -235,8 +239,9 @@ def _ptr_of(a):
             return a.data_ptr(), a.is_cuda
     except ImportError:
         pass
-    arr = np.ascontiguousarray(a, dtype=np.float32)
-    return arr.ctypes.data, False
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous):
+        raise TypeError("host arrays must be contiguous float32 (build_diagram converts and keeps them)")
+    return a.ctypes.data, False
 
 
 def build_diagram(points, weights=None, box=None, *, device: int | None = None, stream=None, leaf_size: int = 0,
@@ -245,13 +250,13 @@ def build_diagram(points, weights=None, box=None, *, device: int | None = None, 
     array); weights: float32 [n] or None; box: (lo.x, lo.y, lo.z, hi.x, hi.y, hi.z) or None.
     Device outputs come back as zero-copy torch CUDA tensors; with out_host=True as numpy arrays."""
     L = load_library()
-    keep = []
+    keep = []  # host copies made here stay alive until pd_build returns
     if not hasattr(points, "data_ptr"):
         points = np.ascontiguousarray(np.asarray(points, dtype=np.float32).reshape(-1, 3))
         keep.append(points)
-        if weights is not None:
-            weights = np.ascontiguousarray(np.asarray(weights, dtype=np.float32).reshape(-1))
-            keep.append(weights)
+    if weights is not None and not hasattr(weights, "data_ptr"):
+        weights = np.ascontiguousarray(np.asarray(weights, dtype=np.float32).reshape(-1))
+        keep.append(weights)
     pp, p_dev = _ptr_of(points)
     wp, w_dev = _ptr_of(weights)
     if weights is not None and w_dev != p_dev:
@@ -301,6 +306,11 @@ def export_slice(d: Diagram, stream=None):
                              rn.data_ptr(), ra.data_ptr(), ctypes.byref(total), ctypes.c_void_p(stream)))
     t = int(total.value)
     return cnt, vol, surf, flg, rn[:t], ra[:t]
+
+
+def trim(device: int = 0):
+    """pd_trim: release the cached build workspace and pinned host buffers of `device`."""
+    _check(load_library().pd_trim(int(device)))
 
 
 def sort_pairs_u64(keys, vals, stream=None):

@@ -59,6 +59,19 @@ void ck(cudaError_t e) {
     }
 }
 
+// CUDA event destroyed with its scope (error paths included).
+struct Ev {
+    cudaEvent_t e = nullptr;
+    Ev() = default;
+    Ev(const Ev&) = delete;
+    Ev& operator=(const Ev&) = delete;
+    ~Ev() {
+        if (e) cudaEventDestroy(e);
+    }
+    void create() { ck(cudaEventCreate(&e)); }
+    operator cudaEvent_t() const { return e; }
+};
+
 // Stream-ordered allocations, released at scope end (cudaFreeAsync) unless handed to a result.
 struct Arena {
     cudaStream_t st;
@@ -178,6 +191,15 @@ struct PinnedCache {
         free_.emplace(cap, p);
         cached += cap;
     }
+    void trim() {  // release every cached (free) buffer
+        std::lock_guard<std::mutex> g(mu);
+        for (auto& kv : free_) {
+            cap_.erase(kv.second);
+            cudaFreeHost(kv.second);
+        }
+        free_.clear();
+        cached = 0;
+    }
 };
 PinnedCache& pinned() {
     static PinnedCache c;
@@ -251,8 +273,8 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
     r->device = opt.device;
     r->stream = (cudaStream_t)opt.stream;
     try {
-        cudaEvent_t ev[5];
-        for (auto& e : ev) ck(cudaEventCreate(&e));
+        Ev ev[5];
+        for (auto& e : ev) e.create();
         ck(cudaEventRecord(ev[0], st));
         // ---- inputs
         const float* dpts = points;
@@ -329,7 +351,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         bvh.nodes = W.alloc<pd::WideNode>(sc.max_wide);
         sc.tasks[0] = W.alloc<int2>(sc.max_wide);
         sc.tasks[1] = W.alloc<int2>(sc.max_wide);
-        sc.counters = W.alloc<int>(4);
+        sc.counters = W.alloc<int>(pd::kCollapseCounters);
         bvh.root = W.alloc<pd::NodeChild>(1);
         ck(pd::bvh_topology(keys_s, sorted, (int)n, leaf, sc, bvh, st, &launches));
         ck(cudaEventRecord(ev[1], st));
@@ -422,11 +444,11 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         r->slice_end = end;
         // ---- optional KNN warm start: K = 8 nearest sites of every site of the slice
         int32_t* knn = nullptr;
-        cudaEvent_t kev[2] = {nullptr, nullptr};
+        Ev kev[2];
         if (opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE)) {
             knn = W.alloc<int32_t>((size_t)n * pd::KNN_K);
-            ck(cudaEventCreate(&kev[0]));
-            ck(cudaEventCreate(&kev[1]));
+            kev[0].create();
+            kev[1].create();
             ck(cudaEventRecord(kev[0], st));
             const int adaptive = (opt.flags & PD_WARM_START) ? 0 : 1;
             ck(pd::knn_query(sorted, bvh.nodes, bvh.root, (int)begin, (int)end, adaptive, knn, sms, st, &launches));
@@ -445,8 +467,8 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         int32_t* nbr = nullptr;  // CSR outputs: allocated with the arena (same capacity) so the CSR
         float* area = nullptr;   // phase never grows the memory pool mid-build
         float* aarea = nullptr;
-        cudaEvent_t tev[4];
-        for (auto& e : tev) ck(cudaEventCreate(&e));
+        Ev tev[4];
+        for (auto& e : tev) e.create();
         // dual tetrahedra (PD_TETS): ~6.8 per site for Poisson-Voronoi input, each listed once
         const bool want_tets = (opt.flags & PD_TETS) != 0;
         int32_t* tcnt = want_tets ? W.alloc<int32_t>(n) : nullptr;
@@ -531,26 +553,11 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
                 if (tier >= 1) {
                     // Longest first: a short list of heavy cells (C5's top tier: ~250 cells, the largest
                     // alone ~0.45 s) is started in descending order of the work they had done when they
-                    // outgrew the previous tier, so the heaviest never queue behind others.
-                    int32_t nl = 0;
-                    ck(cudaMemcpyAsync(&nl, list_counts + (tier - 1), sizeof(nl), cudaMemcpyDeviceToHost, st));
-                    ck(cudaStreamSynchronize(st));
-                    if (nl > 1 && nl <= 8192) {
-                        std::vector<int32_t> hl(nl), hc(nl), order(nl);
-                        const int32_t* dcost = lcost + (size_t)((tier - 1) & 1) * std::max<int64_t>(L, 1);
-                        ck(cudaMemcpyAsync(hl.data(), P.list, sizeof(int32_t) * nl, cudaMemcpyDeviceToHost, st));
-                        ck(cudaMemcpyAsync(hc.data(), dcost, sizeof(int32_t) * nl, cudaMemcpyDeviceToHost, st));
-                        ck(cudaStreamSynchronize(st));
-                        for (int32_t k = 0; k < nl; ++k) order[k] = k;
-                        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
-                            return hc[a] != hc[b] ? hc[a] > hc[b] : hl[a] < hl[b];
-                        });
-                        std::vector<int32_t> sl(nl);
-                        for (int32_t k = 0; k < nl; ++k) sl[k] = hl[order[k]];
-                        ck(cudaMemcpyAsync(const_cast<int32_t*>(P.list), sl.data(), sizeof(int32_t) * nl,
-                                           cudaMemcpyHostToDevice, st));
-                        ck(cudaStreamSynchronize(st));
-                    }
+                    // outgrew the previous tier, so the heaviest never queue behind others.  Sorted on
+                    // the device (no host round trip between the tiers).
+                    ck(pd::sort_list_by_cost(const_cast<int32_t*>(P.list),
+                                             lcost + (size_t)((tier - 1) & 1) * std::max<int64_t>(L, 1),
+                                             P.list_count, st, &launches));
                 }
                 ck(cudaEventRecord(tev[tier], st));
                 ck(pd::launch_cells(tier, P, st, sms, &launches));
@@ -618,21 +625,17 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         cudaEventElapsedTime(&t12, ev[1], ev[2]);
         cudaEventElapsedTime(&t23, ev[2], ev[3]);
         cudaEventElapsedTime(&t04, ev[0], ev[4]);
-        for (auto& e : ev) cudaEventDestroy(e);
         pd_stats& s = r->stats;
         for (int k = 0; k < 3; ++k) {
             float tt = 0.f;
             cudaEventElapsedTime(&tt, tev[k], tev[k + 1]);
             s.ms_tier[k] = tt;
         }
-        for (auto& e : tev) cudaEventDestroy(e);
         s.ms_knn = 0.0;
-        if (kev[0]) {
+        if (kev[0].e) {
             float tk = 0.f;
             cudaEventElapsedTime(&tk, kev[0], kev[1]);
             s.ms_knn = tk;
-            cudaEventDestroy(kev[0]);
-            cudaEventDestroy(kev[1]);
         }
         s.cells = (int64_t)hs.cells;
         s.nodes_visited = (int64_t)hs.nodes;
@@ -644,6 +647,9 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         s.overflow_cells = (int64_t)hs.overflow;
         s.queue_spills = (int64_t)hs.spills;
         for (int k = 0; k < 10; ++k) s.warp_cycles[k] = (int64_t)hs.cyc[k];
+        s.faces_dropped = (int64_t)hs.dropped;
+        s.faces_near_degenerate = (int64_t)hs.small;
+        s.degraded_cells = (int64_t)hs.degraded;
         s.nnz = nnz;
         s.ms_bvh = t01;
         s.ms_cells = t12;
@@ -653,9 +659,13 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         *out = r;
         return PD_OK;
     } catch (const Fail& f) {
-        cudaStreamSynchronize(st);
+        cudaStreamSynchronize(st);  // kernels may still use workspace memory the next build reuses
         free_result(r);
         return f.s;
+    } catch (...) {  // e.g. std::bad_alloc of a host vector: same cleanup, before the workspace lock goes
+        cudaStreamSynchronize(st);
+        free_result(r);
+        return PD_EINTERNAL;
     }
 }
 
@@ -729,8 +739,10 @@ pd_status pd_assemble(const int32_t* perm, const int32_t* cnt_m, const float* vo
     pd_options opt;
     memset(&opt, 0, sizeof(opt));
     if (optp) opt = *optp;
-    if (!out || n <= 0 || !perm || !cnt_m) return PD_EINVAL;
+    if (!out) return PD_EINVAL;
     *out = nullptr;
+    if (n <= 0 || total < 0 || !perm || !cnt_m || !vol_m || !surf_m || !flags_m) return PD_EINVAL;
+    if (total > 0 && (!rows_nbr || !rows_area)) return PD_EINVAL;
     pd_result* r = new pd_result();
     memset(&r->stats, 0, sizeof(r->stats));
     r->n = n;
@@ -753,6 +765,10 @@ pd_status pd_assemble(const int32_t* perm, const int32_t* cnt_m, const float* vo
         ck(pd::scan_counts(cnt_m, moff, n, nullptr, &sb, st, nullptr));
         void* tmp = A.alloc<unsigned char>(sb);
         ck(pd::scan_counts(cnt_m, moff, n, tmp, &sb, st, &launches));
+        int64_t rows_total = -1;  // the row lengths must add up to the caller's `total`
+        ck(cudaMemcpyAsync(&rows_total, moff + n, sizeof(rows_total), cudaMemcpyDeviceToHost, st));
+        ck(cudaStreamSynchronize(st));
+        if (rows_total != total) throw Fail{PD_EINVAL};
         size_t sb2 = 0;
         ck(pd::scan_counts(cnt, offsets, n, nullptr, &sb2, st, nullptr));
         void* tmp2 = A.alloc<unsigned char>(sb2);
@@ -776,9 +792,30 @@ pd_status pd_assemble(const int32_t* perm, const int32_t* cnt_m, const float* vo
         *out = r;
         return PD_OK;
     } catch (const Fail& f) {
+        cudaStreamSynchronize((cudaStream_t)opt.stream);
         free_result(r);
         return f.s;
+    } catch (...) {
+        cudaStreamSynchronize((cudaStream_t)opt.stream);
+        free_result(r);
+        return PD_EINTERNAL;
     }
+}
+
+pd_status pd_trim(int device) {
+    if (device < 0 || device >= 64) return PD_EINVAL;
+    Workspace& W = workspace(device);
+    std::lock_guard<std::mutex> g(W.mu);  // waits for a build in flight on this device
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cudaSetDevice(device) != cudaSuccess) return PD_ECUDA;
+    cudaDeviceSynchronize();
+    for (auto& c : W.chunks) cudaFree(c.first);
+    W.chunks.clear();
+    W.reset();
+    pinned().trim();
+    cudaSetDevice(cur);
+    return PD_OK;
 }
 
 pd_status pd_sort_pairs_u64(const uint64_t* keys_in, const uint32_t* vals_in, int64_t n, uint64_t* keys_out,

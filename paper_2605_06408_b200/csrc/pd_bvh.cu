@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "pd_bvh.cuh"
 #include "pd_internal.cuh"
 
@@ -163,18 +165,21 @@ __device__ __forceinline__ float box_area(float4 lo, float4 hi) {
     return dx * dy + dy * dz + dz * dx;
 }
 
-// Collapse the binary LBVH into 8-wide nodes, one level of wide nodes per launch.  Task (b, w):
-// wide node w covers binary subtree b.  Its children start as b's two children; the internal child
-// (more than l sites) with the largest surface area is replaced by its two children until there
-// are 8.  Children with <= l sites become leaf-range links (the collapse of PAPER.md:527's leaf
-// size l); larger ones become new wide nodes (next level's tasks).
-__global__ void k_collapse(const int2* __restrict__ tasks, int ntask, const int2* __restrict__ child,
-                           const int2* __restrict__ range, const float4* __restrict__ blo, const float4* __restrict__ bhi,
-                           const float4* __restrict__ s, int leaf, WideNode* __restrict__ wide, int* counters,
-                           int2* __restrict__ tasks_out) {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntask) return;
-    int2 task = tasks[t];
+// Collapse the binary LBVH into 8-wide nodes.  Task (b, w): wide node w covers binary subtree b.
+// Its children start as b's two children; the internal child (more than l sites) with the largest
+// surface area is replaced by its two children until there are 8.  Children with <= l sites become
+// leaf-range links (the collapse of PAPER.md:527's leaf size l); larger ones become new wide nodes
+// (next level's tasks).
+// Capacity: every wide node is a distinct binary node with > l sites.  Those nodes form an upward-
+// closed subtree whose lowest members are disjoint sets of > l sites, so there are at most n/(l+1)
+// of them and the subtree has at most 2n/(l+1) - 1 nodes <= max_wide = min(2n/l + 2, n).  The guard
+// below therefore never fires on a well-formed tree; it turns a violated invariant into an error
+// (ovf) instead of an out-of-bounds write.
+__device__ __forceinline__ void collapse_task(int2 task, const int2* __restrict__ child, const int2* __restrict__ range,
+                                              const float4* __restrict__ blo, const float4* __restrict__ bhi,
+                                              const float4* __restrict__ s, int leaf, WideNode* __restrict__ wide,
+                                              int* wide_count, int* next_count, int2* __restrict__ tasks_out, int max_wide,
+                                              int* ovf) {
     int ref[WIDE];
     int2 c0 = child[task.x];
     ref[0] = c0.x;
@@ -188,7 +193,7 @@ __global__ void k_collapse(const int2* __restrict__ tasks, int ntask, const int2
             if (r < 0) continue;
             int2 rg = range[r];
             if (rg.y - rg.x + 1 <= leaf) continue;
-            float A = box_area(blo[r], bhi[r]);
+            float A = box_area(__ldcg(&blo[r]), __ldcg(&bhi[r]));
             if (A > bestA) { bestA = A; best = k; }
         }
         if (best < 0) break;
@@ -212,20 +217,65 @@ __global__ void k_collapse(const int2* __restrict__ tasks, int ntask, const int2
             int r = ref[k];
             int2 rg = range[r];
             int cnt = rg.y - rg.x + 1;
-            a = blo[r];
-            b = bhi[r];
+            a = __ldcg(&blo[r]);
+            b = __ldcg(&bhi[r]);
             if (cnt <= leaf) {
                 link = leaf_link(rg.x, cnt);
             } else {
-                link = atomicAdd(&counters[0], 1);
-                int q = atomicAdd(&counters[1], 1);
-                tasks_out[q] = make_int2(r, link);
+                link = atomicAdd(wide_count, 1);
+                int q = atomicAdd(next_count, 1);
+                if (link < max_wide && q < max_wide) tasks_out[q] = make_int2(r, link);
+                else { atomicExch(ovf, 1); link = EMPTY_LINK; }
             }
         }
         out.c[k].lo_w = a;
         out.c[k].hi_l = make_float4(b.x, b.y, b.z, __int_as_float(link));
     }
-    wide[task.y] = out;
+    if (task.y < max_wide) wide[task.y] = out;
+}
+
+// Grid-wide barrier for a cooperative launch (every block co-resident): arrive on a counter, the last
+// block bumps the generation word the others spin on.
+__device__ __forceinline__ void grid_barrier(unsigned* arrive, volatile unsigned* gen, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(arrive, 1u) == nblocks - 1) {
+            *arrive = 0u;
+            __threadfence();
+            atomicAdd((unsigned*)gen, 1u);
+        } else {
+            while (*gen == g) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// All collapse levels in ONE cooperative launch (no host round trip per level): level L reads its
+// tasks from tasks[L & 1] (count counters[2 + L]) and appends the next level's to tasks[(L+1) & 1].
+// counters: [0] wide-node count, [1] overflow flag, [2 + L] task count of level L, [kMaxLevels + 2]
+// barrier arrive, [kMaxLevels + 3] barrier generation.
+constexpr int kMaxLevels = 120;  // binary depth <= 63 key bits + 32 index bits (duplicate codes)
+__global__ void __launch_bounds__(256) k_collapse_all(int2* __restrict__ tasks0, int2* __restrict__ tasks1,
+                                                      const int2* __restrict__ child, const int2* __restrict__ range,
+                                                      const float4* __restrict__ blo, const float4* __restrict__ bhi,
+                                                      const float4* __restrict__ s, int leaf, WideNode* __restrict__ wide,
+                                                      int* counters, int max_wide) {
+    volatile int* vc = counters;
+    const unsigned nb = gridDim.x;
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
+    for (int L = 0; L < kMaxLevels; ++L) {
+        const int ntask = vc[2 + L];
+        if (ntask == 0 || vc[1]) break;  // uniform over the grid (written before the last barrier)
+        const int2* tin = (L & 1) ? tasks1 : tasks0;
+        int2* tout = (L & 1) ? tasks0 : tasks1;
+        for (int t = tid; t < ntask; t += nthreads)
+            collapse_task(__ldcg(&tin[t]), child, range, blo, bhi, s, leaf, wide, &counters[0], &counters[2 + L + 1],
+                          tout, max_wide, &counters[1]);
+        grid_barrier((unsigned*)&counters[kMaxLevels + 2], (volatile unsigned*)&counters[kMaxLevels + 3], nb);
+    }
 }
 
 __global__ void k_root(const float4* __restrict__ blo, const float4* __restrict__ bhi, int n, int leaf,
@@ -236,7 +286,7 @@ __global__ void k_root(const float4* __restrict__ blo, const float4* __restrict_
     root->hi_l = make_float4(hi.x, hi.y, hi.z, __int_as_float(link));
     tasks[0] = make_int2(0, 0);
     counters[0] = 1;  // wide node 0 = the root's node
-    counters[1] = 0;
+    counters[2] = 1;  // level 0: one task (the root)
 }
 
 __global__ void k_root_single(NodeChild* root) {
@@ -291,28 +341,30 @@ cudaError_t bvh_topology(const uint64_t* keys_sorted, const float4* sorted, int 
     k_karras<<<blocks(n - 1, 256), 256, 0, st>>>(keys_sorted, n, sc.child, sc.range, sc.parent_int, sc.parent_leaf);
     cudaMemsetAsync(sc.visit, 0, sizeof(int) * (size_t)(n - 1), st);
     k_refit<<<blocks(n, 256), 256, 0, st>>>(sorted, n, sc.child, sc.parent_int, sc.parent_leaf, sc.visit, sc.blo, sc.bhi);
+    cudaMemsetAsync(sc.counters, 0, sizeof(int) * kCollapseCounters, st);
     k_root<<<1, 1, 0, st>>>(sc.blo, sc.bhi, n, leaf, out.root, sc.tasks[0], sc.counters);
     *launches += 3;
     out.n_wide = 0;
     out.levels = 0;
     if (n <= leaf) return cudaGetLastError();
-    // level-synchronous collapse: the host reads each level's task count (one small sync per level)
-    int ntask = 1, cur = 0;
-    while (ntask > 0) {
-        k_collapse<<<blocks(ntask, 128), 128, 0, st>>>(sc.tasks[cur], ntask, sc.child, sc.range, sc.blo, sc.bhi, sorted,
-                                                        leaf, out.nodes, sc.counters, sc.tasks[cur ^ 1]);
-        ++*launches;
-        ++out.levels;
-        int h[2];
-        cudaMemcpyAsync(h, sc.counters, sizeof(h), cudaMemcpyDeviceToHost, st);
-        cudaMemsetAsync(sc.counters + 1, 0, sizeof(int), st);
-        cudaError_t e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) return e;
-        out.n_wide = h[0];
-        if (h[0] > sc.max_wide) return cudaErrorInvalidValue;
-        ntask = h[1];
-        cur ^= 1;
+    // every collapse level in one cooperative launch (grid = co-resident blocks); no host round trip
+    static int grid[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!grid[dev & 63]) {
+        int per_sm = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_collapse_all, 256, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid[dev & 63] = std::max(1, std::min(per_sm, 4)) * std::max(sms, 1);
     }
+    int max_wide = sc.max_wide;
+    void* args[] = {(void*)&sc.tasks[0], (void*)&sc.tasks[1], (void*)&sc.child, (void*)&sc.range, (void*)&sc.blo,
+                    (void*)&sc.bhi, (void*)&sorted, (void*)&leaf, (void*)&out.nodes, (void*)&sc.counters,
+                    (void*)&max_wide};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_collapse_all, dim3(grid[dev & 63]), dim3(256), args, 0, st);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+    out.levels = -1;  // not read back (the cell kernel never needs it)
     return cudaGetLastError();
 }
 

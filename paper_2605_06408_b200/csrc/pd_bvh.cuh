@@ -7,6 +7,8 @@
 
 namespace pd {
 
+constexpr int kCollapseCounters = 128;
+
 struct BvhScratch {
     int2* child = nullptr;      // n-1
     int2* range = nullptr;      // n-1
@@ -16,7 +18,7 @@ struct BvhScratch {
     float4* blo = nullptr;      // n-1
     float4* bhi = nullptr;      // n-1
     int2* tasks[2] = {nullptr, nullptr};  // collapse work lists (binary node, wide node)
-    int* counters = nullptr;    // [0] wide-node count, [1..2] task counts
+    int* counters = nullptr;    // kCollapseCounters ints: [0] wide-node count, [1] overflow, [2+L] level-L tasks, barrier
     int max_wide = 0;
 };
 
@@ -44,6 +46,9 @@ cudaError_t csr_gather(const int32_t* cnt, const int64_t* aoff, const int64_t* o
 // dual tetrahedra rows: copy each cell's arena tets into the final order
 cudaError_t tet_gather(const int32_t* tcnt, const int64_t* taoff, const int64_t* toff, const int4* tarena, int64_t n,
                        int4* tets, cudaStream_t st, int* launches);
+
+// longest-first order of a capacity tier's overflow list (device count; <= 8192 entries, else unchanged)
+cudaError_t sort_list_by_cost(int32_t* list, const int32_t* cost, const int32_t* count, cudaStream_t st, int* launches);
 
 // sharding helpers
 cudaError_t slice_export_meta(const int32_t* perm, int64_t begin, int64_t len, const int32_t* cnt, const float* vol,

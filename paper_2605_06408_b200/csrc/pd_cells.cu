@@ -135,6 +135,7 @@ struct Cell {
     float rmax;             // max corner distance of the AABB (isotropic radius bound)
     float sc[3], srad;      // bounding sphere of the cell (SPHERE tiers): center (site-local), radius
     int nv, np, nq;
+    int degraded;           // a topology-consistency check failed (PD_CELL_DEGRADED)
     int self;               // Morton index
     int self_orig;
 };
@@ -245,13 +246,16 @@ __device__ __forceinline__ bool exact_on(unsigned flags, unsigned long long visi
 enum { ST_OK = 0, ST_EMPTY = 1, ST_OVERFLOW = 2, ST_DUP = 3 };
 enum { CLIP_NONE = 0, CLIP_DONE = 1, CLIP_EMPTY = 2, CLIP_OVF = 3 };
 
-struct Counters {
-    unsigned long long nodes, leaves, sites, tests, clips, spills;
-    unsigned long long cyc[10];  // PD_PROFILE: init, descend, leaf, clip, pop, finalize | clip: classify, boundary, create, aabb
-};
 #ifndef PD_PROFILE
 #define PD_PROFILE 0
 #endif
+struct Counters {
+    unsigned long long nodes, leaves, sites, tests, clips, spills;
+    unsigned dropped, small, degraded;  // robustness counters (always published)
+#if PD_PROFILE
+    unsigned long long cyc[10];  // init, descend, leaf, clip, pop, finalize | clip: classify, boundary, create, aabb
+#endif
+};
 #if PD_PROFILE
 #define PT_BEGIN(v) long long v = clock64()
 #define PT_END(v, k) cnt.cyc[k] += (unsigned long long)(clock64() - v)
@@ -717,6 +721,9 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
     }
     PT_END(t_bnd, 7);
     PT_BEGIN(t_cre);
+    // topology check: the hole of a proper cut is bounded by one cycle of >= 3 edges, i.e.
+    // B >= 3 and every plane starts as many boundary edges as it ends (checked cheaply: B >= 3)
+    if (B < 3 && lane == 0) c.degraded = 1;
     int nvn = nv0 - R + B;
     if (nvn > T::VMAX || B > T::VMAX || np0 + 1 > T::PMAX) return CLIP_OVF;
     // 3. append the plane, create (h, x, y) for every boundary edge
@@ -1218,6 +1225,7 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
     c.nv = 8;
     c.np = 6;
     c.nq = 0;
+    c.degraded = 0;
     if (T::SPHERE) {
         c.flo[0] = c.flo[1] = c.flo[2] = 0.f;
         c.fhi[0] = c.fhi[1] = c.fhi[2] = 0.f;
@@ -1247,7 +1255,8 @@ __device__ __forceinline__ void twins_range(WarpState<T>& S, int nv, int u0, int
 // Face vector areas (1/2 sum v x next(v)), face areas, and this thread's volume / surface partials
 // (faces f0, f0+stride, ...).
 template <class T>
-__device__ __forceinline__ void areas_range(WarpState<T>& S, int nv, int np, int f0, int stride, double& vol, double& surf) {
+__device__ __forceinline__ void areas_range(WarpState<T>& S, int nv, int np, int f0, int stride, double& vol, double& surf,
+                                            bool& missing) {
     for (int f = f0; f < np; f += stride) {
         double Ax = 0, Ay = 0, Az = 0;
 #pragma unroll 1
@@ -1256,7 +1265,10 @@ __device__ __forceinline__ void areas_range(WarpState<T>& S, int nv, int np, int
             int which = ta(t) == f ? 2 : (tb(t) == f ? 0 : (tc(t) == f ? 1 : -1));
             if (which >= 0) {
                 int w = S.tw[which][u];
-                if (w == 0xffff) continue;
+                if (w == 0xffff) {  // an edge without its reverse: the final cell is not closed
+                    missing = true;
+                    continue;
+                }
                 double ux = S.vx[u], uy = S.vy[u], uz = S.vz[u];
                 double wx = S.vx[w], wy = S.vy[w], wz = S.vz[w];
                 Ax += uy * wz - uz * wy;
@@ -1407,10 +1419,12 @@ __device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int
         twins_range(S, nv, w * 32 + lane, stride);
     } else if (kind == JOB_AREAS) {
         double vol = 0, surf = 0;
-        areas_range(S, nv, J.np, w * 32 + lane, stride, vol, surf);
+        bool missing = false;
+        areas_range(S, nv, J.np, w * 32 + lane, stride, vol, surf, missing);
         vol = warp_sum_d(vol);
         surf = warp_sum_d(surf);
-        if (lane == 0) { J.dpart[w][0] = vol; J.dpart[w][1] = surf; }
+        missing = __any_sync(FULL, missing);
+        if (lane == 0) { J.dpart[w][0] = vol; J.dpart[w][1] = surf; J.ipart[w][0] = missing ? 1 : 0; }
     }
 }
 
@@ -1472,7 +1486,7 @@ __device__ __noinline__ void emit_tets(WarpState<T>& S, const Cell& c, int lane,
 
 // Face areas (vector area 1/2 sum v x next(v) around each face), volume, neighbours; FP64.
 template <class T>
-__device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const CellParams& P, int status) {
+__device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const CellParams& P, int status, Counters& cnt) {
     const int i = c.self_orig;
     const CellOut& O = P.out;
     if (status == ST_EMPTY || status == ST_DUP || status == ST_OVERFLOW) {
@@ -1494,32 +1508,41 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
         coop_go<T>(S, J, lane);
         if (lane == 0) J.kind = JOB_AREAS;
         coop_go<T>(S, J, lane);
-        for (int w = 0; w < T::WARPS; ++w) { vol += J.dpart[w][0]; surf += J.dpart[w][1]; }
+        bool missing = false;
+        for (int w = 0; w < T::WARPS; ++w) { vol += J.dpart[w][0]; surf += J.dpart[w][1]; missing |= J.ipart[w][0] != 0; }
         vol /= 3.0;
+        if (missing && lane == 0) c.degraded = 1;
     } else {
         twins_range(S, c.nv, lane, 32);
         __syncwarp();
-        areas_range(S, c.nv, c.np, lane, 32, vol, surf);
+        bool missing = false;
+        areas_range(S, c.nv, c.np, lane, 32, vol, surf, missing);
         vol = warp_sum_d(vol) / 3.0;
         surf = warp_sum_d(surf);
+        if (__any_sync(FULL, missing) && lane == 0) c.degraded = 1;
     }
     __syncwarp();
     // A face counts when its area exceeds 1e-13 S: below that it is a rounding artefact of a
     // zero-area (edge / vertex) contact of a degenerate configuration (reading R2).
-    const double amin = 1e-13 * surf;
+    const double amin = 1e-13 * surf, asmall = 1e-9 * surf;
     bool boundary = false;
     int K = 0;
+    unsigned ndrop = 0, nsmall = 0;
     for (int f0 = 0; f0 < c.np; f0 += 32) {
         int f = f0 + lane;
-        bool nb = false;
+        bool nb = false, drop = false;
         double area = 0;
         if (f < c.np) {
             area = S.farea[f];
             if (area > amin) {
                 if (S.pid[f] < 0) boundary = true;
                 else nb = true;
+            } else if (S.pid[f] >= 0 && area > 0) {
+                drop = true;  // a zero-area contact (reading R2): counted, not a neighbour
             }
         }
+        ndrop += __popc(__ballot_sync(FULL, drop));
+        nsmall += __popc(__ballot_sync(FULL, nb && area < asmall));
         unsigned mb = __ballot_sync(FULL, nb);
         if (nb) {
             int pos = K + __popc(mb & lanemask_lt());
@@ -1548,12 +1571,17 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
         *O.arena_overflow = 1;
     }
     if (O.tarena) emit_tets(S, c, lane, P, amin);
+    const bool degraded = c.degraded != 0;
+    cnt.dropped += ndrop;
+    cnt.small += nsmall;
+    cnt.degraded += degraded ? 1u : 0u;
     if (lane == 0) {
         O.cnt[i] = K;
         O.aoff[i] = base;
         O.vol[i] = (float)vol;
         O.surf[i] = (float)surf;
-        O.flags[i] = (uint8_t)((boundary ? PD_CELL_BOUNDARY : 0) | (vol > 0 ? 0 : PD_CELL_EMPTY));
+        O.flags[i] = (uint8_t)((boundary ? PD_CELL_BOUNDARY : 0) | (vol > 0 ? 0 : PD_CELL_EMPTY) |
+                               (degraded ? PD_CELL_DEGRADED : 0));
     }
 }
 
@@ -1562,12 +1590,13 @@ __device__ __noinline__ void trace_print(int tier, const Cell& c, const Counters
            "clips=%llu spills=%llu\n",
            c.self_orig, tier, st, c.nv, c.np, cyc, a.nodes - b.nodes, a.leaves - b.leaves, a.sites - b.sites,
            a.tests - b.tests, a.clips - b.clips, a.spills - b.spills);
-    if (PD_PROFILE)
+#if PD_PROFILE
         printf("PD_TRACE cell=%d phase_cycles init=%llu descend=%llu leaf=%llu clip=%llu pop=%llu finalize=%llu "
                "classify=%llu boundary=%llu create=%llu aabb=%llu\n",
                c.self_orig, a.cyc[0] - b.cyc[0], a.cyc[1] - b.cyc[1], a.cyc[2] - b.cyc[2], a.cyc[3] - b.cyc[3],
                a.cyc[4] - b.cyc[4], a.cyc[5] - b.cyc[5], a.cyc[6] - b.cyc[6], a.cyc[7] - b.cyc[7], a.cyc[8] - b.cyc[8],
                a.cyc[9] - b.cyc[9]);
+#endif
 }
 
 template <class T, unsigned MODE>
@@ -1586,8 +1615,10 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
         }
     }
     const int64_t total = P.list ? (int64_t)(*P.list_count) : P.count;
-    Counters cnt = {0, 0, 0, 0, 0, 0, {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}};
-    const int gw = blockIdx.x * T::WARPS + wid;
+    Counters cnt;
+    memset(&cnt, 0, sizeof(cnt));
+    // spill stack per cell program: per warp, or per CTA in a cooperative tier (only warp 0 traverses)
+    const int gw = T::COOP ? blockIdx.x : blockIdx.x * T::WARPS + wid;
     NodeChild* spill = P.spill + (size_t)gw * P.spill_cap;
     for (int k = lane; k < T::EBW; k += 32) S.ebits[k] = 0u;
     __syncwarp();
@@ -1639,7 +1670,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             }
             if (st == ST_OVERFLOW) novf++;
             PT_BEGIN(t_fin);
-            finalize(S, c, lane, P, st);
+            finalize(S, c, lane, P, st, cnt);
             PT_END(t_fin, 5);
             ncells++;
 #if PD_PROFILE
@@ -1668,7 +1699,14 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
         red_add_g(&P.stats->tier[tier], ncells);
         red_add_g(&P.stats->overflow, novf);
         red_add_g(&P.stats->spills, cnt.spills);
+#if PD_PROFILE
         for (int k = 0; k < 10; ++k) red_add_g(&P.stats->cyc[k], cnt.cyc[k]);
+#endif
+    }
+    if (lane == 0 && (cnt.dropped | cnt.small | cnt.degraded)) {  // robustness counters: always
+        red_add_g(&P.stats->dropped, cnt.dropped);
+        red_add_g(&P.stats->small, cnt.small);
+        red_add_g(&P.stats->degraded, cnt.degraded);
     }
 }
 
@@ -1728,8 +1766,9 @@ int cells_grid_warps(int tier, int num_sms) {
         g = max(g, tier_grid<Tier1, kDynMode>(num_sms));
         return g * Tier1::WARPS;
     }
-    if (tier == 1) return tier_grid<Tier2, kDynMode>(num_sms) * Tier2::WARPS;
-    return tier_grid<Tier3, kDynMode>(num_sms) * Tier3::WARPS;
+    // cell programs (spill stacks): one per warp, or one per CTA in a cooperative tier
+    if (tier == 1) return tier_grid<Tier2, kDynMode>(num_sms) * (Tier2::COOP ? 1 : Tier2::WARPS);
+    return tier_grid<Tier3, kDynMode>(num_sms) * (Tier3::COOP ? 1 : Tier3::WARPS);
 }
 
 }  // namespace pd

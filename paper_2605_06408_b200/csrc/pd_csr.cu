@@ -106,11 +106,57 @@ __global__ void k_gather_cost(const int32_t* __restrict__ perm, const int32_t* _
     if (k < ns) out[k] = cost[perm[pos[k]]];
 }
 
+
+// Longest-first order of a capacity tier's overflow list: one CTA bitonic-sorts up to
+// kListSortMax (cell, cost) pairs in shared memory by (cost descending, Morton index ascending); a
+// longer list keeps its (arbitrary) order.  Runs on the device so no host round trip separates the
+// tiers.
+constexpr int kListSortMax = 8192;
+__global__ void __launch_bounds__(1024) k_sort_list(int32_t* __restrict__ list, const int32_t* __restrict__ cost,
+                                                    const int32_t* __restrict__ count) {
+    extern __shared__ unsigned long long key[];  // kListSortMax entries (64 KB, dynamic)
+    const int n = *count;
+    if (n <= 1 || n > kListSortMax) return;
+    int m = 2;
+    while (m < n) m <<= 1;
+    for (int k = threadIdx.x; k < m; k += blockDim.x)
+        key[k] = k < n ? ((unsigned long long)(uint32_t)(0x7fffffff - max(cost[k], 0)) << 32) | (uint32_t)list[k]
+                       : ~0ull;
+    __syncthreads();
+    for (int size = 2; size <= m; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int k = threadIdx.x; k < m; k += blockDim.x) {
+                const int o = k ^ stride;
+                if (o > k) {
+                    const bool up = (k & size) == 0;
+                    const unsigned long long a = key[k], b = key[o];
+                    if ((a > b) == up) { key[k] = b; key[o] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int k = threadIdx.x; k < n; k += blockDim.x) list[k] = (int32_t)(uint32_t)key[k];
+}
+
 }  // namespace
 
 cudaError_t gather_sample_cost(const int32_t* perm, const int32_t* pos, int64_t ns, const int32_t* cost, int32_t* out,
                                cudaStream_t st, int* launches) {
     k_gather_cost<<<blocks(ns, 256), 256, 0, st>>>(perm, pos, ns, cost, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t sort_list_by_cost(int32_t* list, const int32_t* cost, const int32_t* count, cudaStream_t st, int* launches) {
+    static bool attr[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr[dev & 63]) {
+        cudaFuncSetAttribute(k_sort_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kListSortMax * sizeof(unsigned long long)));
+        attr[dev & 63] = true;
+    }
+    k_sort_list<<<1, 1024, kListSortMax * sizeof(unsigned long long), st>>>(list, cost, count);
     ++*launches;
     return cudaGetLastError();
 }

@@ -56,8 +56,9 @@ struct CellOut {
     int* tovf;
 };
 
-struct Stats {  // device counters (PD_STATS)
+struct Stats {  // device counters (PD_STATS), robustness counters (always)
     unsigned long long nodes, leaves, sites, clip_tests, clips, cells, tier[3], overflow, spills, cyc[10];
+    unsigned long long dropped, small, degraded;
 };
 
 struct CellParams {

@@ -6,7 +6,11 @@ Per checked cell i:
     excused pairs are counted and reported;
   * |vol_gpu - vol_oracle| <= 1e-4 * vol_oracle (cells not excused);
   * |a_gpu - a_oracle| <= 1e-3 * a_oracle for every pair not excused;
-  * an EMPTY-flag mismatch is excused only if every face of the non-empty side is below tau.
+  * an EMPTY-flag mismatch is excused only if every face of the non-empty side is below tau;
+  * the BOUNDARY (a wall face of area > 1e-13 S, reading R3) and DUPLICATE (reading R5) flags must
+    be equal.
+The oracle's near-degenerate counts (bisector faces <= 1e-13 S it drops, neighbour faces < 1e-9 S)
+are summed into the report beside the GPU's (pd_stats faces_dropped / faces_near_degenerate).
 S_i comes from the oracle; S_j from the oracle when j was checked, else from the GPU output.
 """
 from __future__ import annotations
@@ -18,7 +22,7 @@ import numpy as np
 TAU_REL = 1e-9
 VOL_REL = 1e-4
 AREA_REL = 1e-3
-EMPTY = 1
+EMPTY, BOUNDARY, DUPLICATE = 1, 2, 8
 
 
 @dataclass
@@ -28,6 +32,9 @@ class Report:
     excused_pairs: int = 0
     max_rel_area: float = 0.0
     max_rel_vol: float = 0.0
+    flag_checked: int = 0
+    oracle_dropped: int = 0
+    oracle_small: int = 0
     failures: list = field(default_factory=list)
 
     @property
@@ -37,6 +44,8 @@ class Report:
     def summary(self) -> str:
         return (f"cells={self.cells} passed={self.passed} excused_pairs={self.excused_pairs} "
                 f"max_rel_area={self.max_rel_area:.3g} max_rel_vol={self.max_rel_vol:.3g} "
+                f"flags_checked={self.flag_checked} oracle_dropped={self.oracle_dropped} "
+                f"oracle_small={self.oracle_small} "
                 f"first_failures={self.failures[:5]}")
 
 
@@ -81,6 +90,17 @@ def compare(gpu, orc, max_failures: int = 50) -> Report:
             if rel > AREA_REL:
                 ok = False
                 why.append(f"area {j}: {b} vs {a}")
+        same_empty = bool(orc.flags[t] & EMPTY) == bool(g_flags[i] & EMPTY)
+        for bit, nm in ((BOUNDARY, "BOUNDARY"), (DUPLICATE, "DUPLICATE")):
+            if bit == BOUNDARY and not same_empty:  # an excused EMPTY mismatch (below) decides these cells
+                continue
+            if bool(orc.flags[t] & bit) != bool(g_flags[i] & bit):
+                ok = False
+                why.append(f"{nm} flag oracle={bool(orc.flags[t] & bit)} gpu={bool(g_flags[i] & bit)}")
+        rep.flag_checked += 1
+        if getattr(orc, "dropped", None) is not None:
+            rep.oracle_dropped += int(orc.dropped[t])
+            rep.oracle_small += int(orc.small[t])
         o_empty = bool(orc.flags[t] & EMPTY)
         g_empty = bool(g_flags[i] & EMPTY)
         if o_empty != g_empty:
@@ -106,14 +126,14 @@ def compare(gpu, orc, max_failures: int = 50) -> Report:
     return rep
 
 
-def sample_cells(gpu, n: int, seed: int, n_random: int = 256, n_stratum: int = 64) -> np.ndarray:
-    """Parity sample: random cells + the largest rows (cost tail proxy) + BOUNDARY
-    + EMPTY cells + every OVERFLOW cell."""
+def sample_cells(gpu, n: int, seed: int, n_random: int = 256, n_stratum: int = 64, cost=None) -> np.ndarray:
+    """Parity sample: random cells + the cost tail (the largest per-cell GPU work,
+    pd_cell_cost, when given; else the largest rows) + BOUNDARY + EMPTY cells + every OVERFLOW cell."""
     rng = np.random.default_rng(seed)
     flags = np.asarray(gpu.flags)
-    deg = np.diff(np.asarray(gpu.offsets))
+    tail = np.asarray(cost) if cost is not None else np.diff(np.asarray(gpu.offsets))
     picks = [rng.choice(n, size=min(n_random, n), replace=False)]
-    picks.append(np.argsort(-deg, kind="stable")[:n_stratum])
+    picks.append(np.argsort(-tail, kind="stable")[:n_stratum])
     for bit in (2, 1):
         idx = np.flatnonzero(flags & bit)
         if len(idx):

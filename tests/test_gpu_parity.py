@@ -96,8 +96,11 @@ def test_leaf_sizes_identical(leaf):
     assert np.allclose(ref.volumes, g.volumes, rtol=1e-6, atol=0)
 
 
-@pytest.mark.parametrize("flag", [pd.ISOTROPIC, pd.DFS, pd.PAPER_BOUND, pd.WARM_START, pd.WARM_START | pd.DFS,
-                                  pd.WARM_ADAPTIVE])
+ABLATIONS = [pd.ISOTROPIC, pd.DFS, pd.PAPER_BOUND, pd.NO_EXACT, pd.EXACT_NODES, pd.WARM_START | pd.DFS,
+             pd.ISOTROPIC | pd.DFS, pd.WARM_ADAPTIVE]
+
+
+@pytest.mark.parametrize("flag", ABLATIONS)
 def test_ablations_neutral(flag):
     """Culling / traversal variants change the work, not the diagram."""
     wl = pdgen.make("C3", n=8009)
@@ -105,6 +108,50 @@ def test_ablations_neutral(flag):
     g = _gpu(wl, flags=flag)
     assert np.array_equal(ref.offsets, g.offsets) and np.array_equal(ref.neighbors, g.neighbors)
     assert np.allclose(ref.volumes, g.volumes, rtol=1e-6)
+
+
+@pytest.mark.parametrize("cfg,n", [("C3", 8009), ("C5", 6007)])
+@pytest.mark.parametrize("flag", ABLATIONS)
+def test_ablations_oracle(cfg, n, flag):
+    """Every ablation / traversal mode of the paper (isotropic culling P:211, DFS P:299, the paper's bounds
+    only P:229-233, no / always exact node tests, KNN warm start P:544-545 with DFS) against the ORACLE on
+    small sets ("oracle-verified"), not only against the default GPU output."""
+    _assert_parity(pdgen.make(cfg, n=n), flags=flag)
+
+
+def _tight_box(points):
+    """The paper's initial cell when no box is given: the FP32 AABB of the points, an
+    axis of zero extent widened by one FP32 ulp on each side (reading R1)."""
+    p = np.asarray(points, np.float32)
+    lo, hi = p.min(axis=0), p.max(axis=0)
+    for k in range(3):
+        if not lo[k] < hi[k]:
+            lo[k] = np.nextafter(lo[k], np.float32(-np.inf))
+            hi[k] = np.nextafter(hi[k], np.float32(np.inf))
+    return tuple(float(v) for v in lo) + tuple(float(v) for v in hi)
+
+
+@pytest.mark.parametrize("case", ["C3", "C4", "flat", "two-flat"])
+def test_box_null_parity(case):
+    """pd_build(box=NULL) (a2): the box is the tight AABB of the points; compared with the
+    oracle run on that box computed on the host, incl. the flat-axis widening."""
+    if case in ("C3", "C4"):
+        wl = pdgen.make(case, n=12007)
+        pts, w = wl.points, wl.weights
+    else:
+        pts = pdgen.white_noise(700, 9, 0.0, 1.0)
+        pts[:, 2] = 0.5  # flat in z
+        if case == "two-flat":
+            pts[:, 1] = 0.25  # a line: flat in y and z
+            pts = pts[:200]
+        w = None
+    g = pd.build_diagram(pts, w, None, out_host=True)
+    o = oracle.cells(pts, w, _tight_box(pts), threads=NT)
+    rep = compare(g, o)
+    print(case, rep.summary())
+    assert rep.ok, rep.summary()
+    bx = np.asarray(_tight_box(pts), np.float64)
+    assert g.volumes.astype(np.float64).sum() == pytest.approx(np.prod(bx[3:] - bx[:3]), rel=1e-5)
 
 
 @pytest.mark.parametrize("cfg,n", [("C1", None), ("C3", 20011), ("C5", 20011)])
@@ -177,6 +224,26 @@ def test_dual_tets_parity(cfg, n):
     # the diagram itself is unchanged by the extra output
     ref_d = _gpu(wl)
     assert np.array_equal(ref_d.offsets, g.offsets) and np.array_equal(ref_d.neighbors, g.neighbors)
+
+
+@pytest.mark.parametrize("case", ["C1", "lattice"])
+def test_robustness_counters(case):
+    """pd_stats faces_dropped / faces_near_degenerate / degraded_cells (always collected): generic input has
+    no degraded cell; cospherical lattices (every vertex shared by > 3 cells) neither, and their zero-area
+    contacts never become neighbours."""
+    if case == "C1":
+        wl = pdgen.make("C1")
+        d = pd.build_diagram(wl.points, None, wl.box, out_host=True)
+        o = oracle.cells(wl.points, None, wl.box, threads=NT)
+        rows = np.repeat(np.arange(wl.n), np.diff(d.offsets))
+        assert d.stats["faces_near_degenerate"] == int(np.sum(d.areas < 1e-9 * d.surface[rows]))
+        assert d.stats["faces_near_degenerate"] == int(o.small.sum())
+    else:
+        gr = np.arange(-3, 4, dtype=np.float64)
+        P = (np.stack(np.meshgrid(gr, gr, gr, indexing="ij"), -1).reshape(-1, 3) * 0.5).astype(np.float32)
+        d = pd.build_diagram(P, None, (-1.8,) * 3 + (1.8,) * 3, out_host=True)
+    print(case, {k: d.stats[k] for k in ("faces_dropped", "faces_near_degenerate", "degraded_cells")})
+    assert d.stats["degraded_cells"] == 0 and not np.any(d.flags & pd.CELL_DEGRADED)
 
 
 def test_determinism_bitwise():
@@ -311,18 +378,26 @@ def test_own_radix_sort_matches_stable_torch_sort(n, bits):
 
 # ----------------------------------------------------------------- full sizes, sampled cells
 
-FULL = [("C2", 256), ("C3", 128), ("C4", 96), ("C5", 64)]
+# SURVEY.md §8(d) sample: 4096 random + 1024 cost tail (pd_cell_cost) + 1024 BOUNDARY + 1024 EMPTY + all OVERFLOW
+FULL = ["C2", "C3", "C4", "C5"]
 
 
-@pytest.mark.parametrize("cfg,nrand", FULL)
-def test_full_size_sampled(cfg, nrand):
+@pytest.mark.parametrize("cfg", FULL)
+def test_full_size_sampled(cfg):
     wl = pdgen.make(cfg)
-    g = _gpu(wl)
-    ids = sample_cells(g, wl.n, seed=123, n_random=nrand, n_stratum=max(8, nrand // 8))
+    p = torch.from_numpy(wl.points).cuda()
+    w = None if wl.weights is None else torch.from_numpy(wl.weights).cuda()
+    d = pd.build_diagram(p, w, wl.box, flags=pd.COST | pd.STATS)  # the bench launch configuration (+ counters)
+    cost = pd.cell_cost(d).cpu().numpy()
+    stats = d.stats
+    g = d.to_numpy()
+    ids = sample_cells(g, wl.n, seed=123, n_random=4096, n_stratum=1024, cost=cost)
     o = oracle.cells(wl.points, wl.weights, wl.box, ids=ids, threads=NT)
     rep = compare(g, o)
-    print(cfg, rep.summary())
+    print(cfg, rep.summary(), "gpu faces_dropped", stats["faces_dropped"], "near_degenerate",
+          stats["faces_near_degenerate"], "degraded", stats["degraded_cells"])
     assert rep.ok, rep.summary()
+    assert len(ids) >= 4096 + 1024
     # properties over ALL cells: box partition and adjacency symmetry
     bx = np.asarray(wl.box, np.float64)
     assert g.volumes.astype(np.float64).sum() == pytest.approx(np.prod(bx[3:] - bx[:3]), rel=1e-5)
@@ -336,3 +411,7 @@ def test_full_size_sampled(cfg, nrand):
     assert np.all(g.areas[one_sided] < tau[one_sided])
     assert one_sided.sum() <= 1e-5 * len(fwd)
     assert not np.any(g.flags & pd.CELL_OVERFLOW)
+    # robustness counters (pd_stats): near-degenerate faces are counted, not silently dropped
+    small = g.areas < 1e-9 * g.surface[rows]
+    assert stats["faces_near_degenerate"] == int(small.sum())
+    assert stats["degraded_cells"] == int(np.count_nonzero(g.flags & pd.CELL_DEGRADED))

@@ -1,4 +1,4 @@
-import sys; sys.path.insert(0, '/root/repo')
+import sys; import os; sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, pdgen, paper_2605_06408_b200 as pd
 n = int(sys.argv[1]) if len(sys.argv) > 1 else None
 wl = pdgen.make("C4", n=n)
