@@ -47,7 +47,7 @@ typedef enum {
     PD_EOUTSIDE = 4,    /* a point lies outside the closed box; pd_error_index() names it */
     PD_ENOMEM = 5,      /* device or host allocation failed */
     PD_ECUDA = 6,       /* a CUDA runtime error (message via pd_last_cuda_error()) */
-    PD_ENCCL = 7,       /* reserved (collectives live in the Python layer, torch.distributed) */
+    PD_ENCCL = 7,       /* an NCCL call failed, or libnccl.so.2 is missing (message via pd_last_nccl_error()) */
     PD_EINTERNAL = 8    /* an internal invariant failed (e.g. output arena overflow twice) */
 } pd_status;
 
@@ -185,6 +185,49 @@ pd_status pd_export_slice(const pd_result* r, int32_t* cnt, float* vol, float* s
                           uint8_t* flags, int32_t* rows_nbr, float* rows_area, int64_t* total,
                           void* stream);
 int64_t pd_slice_nnz(const pd_result* r);
+
+/* ---- Multi-GPU (the paper itself is single-GPU; the sharding rests on the n
+ * independent clipping tasks of PAPER.md:151).  One process per GPU; NCCL (libnccl.so.2, opened at the first
+ * call) over NVLink/NVSwitch inside the library, torch.distributed (or any channel) only to hand the 128-byte
+ * unique id from rank 0 to the others. */
+typedef struct pd_comm pd_comm;
+
+/* Rank 0 creates the communicator's unique id (an ncclUniqueId, 128 bytes) and sends the bytes to the other
+ * ranks by any means.  Errors: PD_EINVAL (uid NULL), PD_ENCCL. */
+pd_status pd_comm_unique_id(unsigned char uid[128]);
+
+/* Collective over `world` ranks: join the communicator of `uid` as `rank` on CUDA device `device`.
+ * *comm receives the handle (release with pd_comm_free after the last pd_build_sharded).
+ * Errors: PD_EINVAL (rank/world/device out of range, NULL), PD_ECUDA, PD_ENCCL. */
+pd_status pd_comm_init(const unsigned char uid[128], int rank, int world, int device, pd_comm** comm);
+
+/* Collective: the diagram of n sites built by all ranks of `comm` together.
+ *  points/weights/box : as pd_build, read on RANK 0 ONLY (other ranks may pass NULL); every rank passes the
+ *                       same n.  opt->device is ignored (the communicator's device is used); PD_TETS is
+ *                       not available (PD_EINVAL).
+ * Rank 0 packs and validates the input and builds the LBVH; NCCL broadcasts a header (status, n, box) and the
+ * LBVH -- Morton-sorted sites (16 B/site), the permutation (4 B/site) and the wide nodes -- to every rank.
+ * Each rank builds the cells of its contiguous slice of the Morton order (equal count, or equal estimated cost
+ * with PD_BALANCE); the per-cell fields and rows of every slice are then broadcast by their owner (grouped
+ * NCCL broadcasts) and EVERY rank assembles the full original-order CSR into *out (same accessors as
+ * pd_build; pd_slice_begin/end give this rank's slice).  The result is byte-identical to pd_build's.
+ * Errors: as pd_build (an input error found on rank 0 is returned by every rank, with pd_error_index),
+ *         PD_EINVAL (n differs from rank 0's, comm NULL), PD_ENCCL. */
+pd_status pd_build_sharded(pd_comm* comm, const float* points, const float* weights, int64_t n, const pd_box* box,
+                           const pd_options* opt, pd_result** out);
+
+int pd_comm_rank(const pd_comm* comm);
+int pd_comm_world(const pd_comm* comm);
+void pd_comm_free(pd_comm* comm);
+const char* pd_last_nccl_error(void); /* thread-local message of the last PD_ENCCL */
+
+/* ---- Roofline denominators measured on the box (bench.py, not the hot path). */
+/* FP32 FFMA throughput in lane-ops/s (one FFMA = one lane-op): best of `reps` launches of independent FFMA
+ * chains at full occupancy.  Errors: PD_EINVAL, PD_ECUDA. */
+pd_status pd_measure_fp32_peak(int device, int reps, double* lane_ops_per_s);
+/* L2 read bandwidth in bytes/s: `bytes` (>= 1 MiB; <= 64 MiB to stay L2-resident) swept 32 times per launch
+ * with L1-bypassing 16-byte loads after a warming launch; best of `reps`.  Errors: PD_EINVAL, PD_ECUDA. */
+pd_status pd_measure_l2_peak(int device, int64_t bytes, int reps, double* bytes_per_s);
 
 /* Test hook for the path's own LSD radix sort: stable sort of n (key < 2^64,
  * value) pairs, all DEVICE pointers on the current device, enqueued on `stream` and synchronized.

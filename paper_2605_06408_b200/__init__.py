@@ -30,7 +30,9 @@ EXPORTED = ["pd_build", "pd_num_cells", "pd_nnz", "pd_on_host", "pd_offsets", "p
             "pd_volumes", "pd_surface", "pd_cell_flags", "pd_cell_cost", "pd_get_stats", "pd_free", "pd_slice_begin",
             "pd_slice_end", "pd_morton_perm", "pd_assemble", "pd_export_slice", "pd_slice_nnz",
             "pd_strerror", "pd_error_index", "pd_last_cuda_error", "pd_abi_version", "pd_last_launch_count",
-            "pd_sort_pairs_u64", "pd_num_tets", "pd_tets", "pd_trim"]
+            "pd_sort_pairs_u64", "pd_num_tets", "pd_tets", "pd_trim", "pd_comm_unique_id", "pd_comm_init",
+            "pd_build_sharded", "pd_comm_free", "pd_comm_rank", "pd_comm_world", "pd_last_nccl_error",
+            "pd_measure_fp32_peak", "pd_measure_l2_peak"]
 
 
 class PdError(RuntimeError):
@@ -105,6 +107,23 @@ def load_library(path: str | None = None):
     L.pd_last_launch_count.restype = I64
     L.pd_trim.restype = ctypes.c_int
     L.pd_trim.argtypes = [ctypes.c_int]
+    L.pd_comm_unique_id.restype = ctypes.c_int
+    L.pd_comm_unique_id.argtypes = [P]
+    L.pd_comm_init.restype = ctypes.c_int
+    L.pd_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P)]
+    L.pd_build_sharded.restype = ctypes.c_int
+    L.pd_build_sharded.argtypes = [P, P, P, I64, P, P, ctypes.POINTER(P)]
+    L.pd_comm_free.restype = None
+    L.pd_comm_free.argtypes = [P]
+    L.pd_comm_rank.restype = ctypes.c_int
+    L.pd_comm_rank.argtypes = [P]
+    L.pd_comm_world.restype = ctypes.c_int
+    L.pd_comm_world.argtypes = [P]
+    L.pd_last_nccl_error.restype = ctypes.c_char_p
+    L.pd_measure_fp32_peak.restype = ctypes.c_int
+    L.pd_measure_fp32_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    L.pd_measure_l2_peak.restype = ctypes.c_int
+    L.pd_measure_l2_peak.argtypes = [ctypes.c_int, I64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     if hasattr(L, "pd_tets"):
         L.pd_num_tets.restype = I64
         L.pd_num_tets.argtypes = [P]
@@ -128,6 +147,8 @@ def _check(status: int):
         idx = int(L.pd_error_index()) if status in (PD_ENONFINITE, PD_EOUTSIDE) else -1
         if status == PD_ECUDA:
             msg += ": " + L.pd_last_cuda_error().decode()
+        if status == PD_ENCCL:
+            msg += ": " + L.pd_last_nccl_error().decode()
         if idx >= 0:
             msg += f" (point {idx})"
         raise PdError(status, msg, idx)
@@ -244,14 +265,10 @@ def _ptr_of(a):
     return a.ctypes.data, False
 
 
-def build_diagram(points, weights=None, box=None, *, device: int | None = None, stream=None, leaf_size: int = 0,
-                  flags: int = 0, out_host: bool = False, shard_rank: int = 0, shard_world: int = 1) -> Diagram:
-    """pd_build (include/pd.h).  points: float32 [n,3] (torch CUDA tensor => device input, else host
-    array); weights: float32 [n] or None; box: (lo.x, lo.y, lo.z, hi.x, hi.y, hi.z) or None.
-    Device outputs come back as zero-copy torch CUDA tensors; with out_host=True as numpy arrays."""
-    L = load_library()
-    keep = []  # host copies made here stay alive until pd_build returns
-    if not hasattr(points, "data_ptr"):
+def _prepare(points, weights, box, device, stream, leaf_size, flags, out_host, shard_rank=0, shard_world=1):
+    """Marshal pd_build's arguments (no arithmetic): returns (keep, pp, wp, n, opt, bx, stream)."""
+    keep = []  # host copies made here stay alive until the C call returns
+    if points is not None and not hasattr(points, "data_ptr"):
         points = np.ascontiguousarray(np.asarray(points, dtype=np.float32).reshape(-1, 3))
         keep.append(points)
     if weights is not None and not hasattr(weights, "data_ptr"):
@@ -259,16 +276,17 @@ def build_diagram(points, weights=None, box=None, *, device: int | None = None, 
         keep.append(weights)
     pp, p_dev = _ptr_of(points)
     wp, w_dev = _ptr_of(weights)
-    if weights is not None and w_dev != p_dev:
+    if weights is not None and points is not None and w_dev != p_dev:
         raise ValueError("points and weights must both be on the device or both on the host")
-    n = int(points.shape[0])
+    n = int(points.shape[0]) if points is not None else 0
     opt = _Options()
     if device is None:
         device = points.device.index if (p_dev and points.device.index is not None) else 0
     opt.device = int(device)
-    if stream is None and p_dev:
+    if stream is None and (p_dev or points is None):
         import torch
-        stream = torch.cuda.current_stream(device).cuda_stream
+        if torch.cuda.is_available():
+            stream = torch.cuda.current_stream(device).cuda_stream
     opt.stream = ctypes.c_void_p(int(stream) if stream else 0)
     opt.leaf_size = int(leaf_size)
     opt.flags = int(flags) | (IN_DEVICE if p_dev else 0) | (OUT_HOST if out_host else 0)
@@ -278,9 +296,68 @@ def build_diagram(points, weights=None, box=None, *, device: int | None = None, 
     if box is not None:
         b = [float(v) for v in box]
         bx = _Box((ctypes.c_float * 3)(*b[:3]), (ctypes.c_float * 3)(*b[3:]))
+    return keep, pp, wp, n, opt, bx, stream
+
+
+def build_diagram(points, weights=None, box=None, *, device: int | None = None, stream=None, leaf_size: int = 0,
+                  flags: int = 0, out_host: bool = False, shard_rank: int = 0, shard_world: int = 1) -> Diagram:
+    """pd_build (include/pd.h).  points: float32 [n,3] (torch CUDA tensor => device input, else host
+    array); weights: float32 [n] or None; box: (lo.x, lo.y, lo.z, hi.x, hi.y, hi.z) or None.
+    Device outputs come back as zero-copy torch CUDA tensors; with out_host=True as numpy arrays."""
+    L = load_library()
+    keep, pp, wp, n, opt, bx, stream = _prepare(points, weights, box, device, stream, leaf_size, flags, out_host,
+                                                shard_rank, shard_world)
     out = ctypes.c_void_p()
     status = L.pd_build(pp, wp, n, ctypes.byref(bx) if bx is not None else None, ctypes.byref(opt),
                         ctypes.byref(out))
+    del keep
+    _check(status)
+    return _wrap(out.value, stream)
+
+
+class Comm:
+    """pd_comm (include/pd.h): an NCCL communicator inside libpd, one rank per GPU."""
+
+    def __init__(self, uid: bytes, rank: int, world: int, device: int):
+        L = load_library()
+        if len(uid) != 128:
+            raise ValueError("unique id must be 128 bytes")
+        buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+        self.ptr = ctypes.c_void_p()
+        _check(L.pd_comm_init(buf, int(rank), int(world), int(device), ctypes.byref(self.ptr)))
+        self.rank, self.world, self.device = int(rank), int(world), int(device)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_ubyte * 128)()
+        _check(load_library().pd_comm_unique_id(buf))
+        return bytes(buf)
+
+    def close(self):
+        if self.ptr and self.ptr.value and _lib is not None:
+            _lib.pd_comm_free(self.ptr)
+        self.ptr = None
+
+    def __del__(self):
+        self.close()
+
+
+def build_sharded(comm: Comm, points, weights=None, box=None, *, n: int | None = None, stream=None,
+                  leaf_size: int = 0, flags: int = 0, out_host: bool = False) -> Diagram:
+    """pd_build_sharded: collective over the ranks of `comm`.  points/weights/box are read on rank 0 only
+    (other ranks may pass None together with n); every rank returns the full diagram."""
+    L = load_library()
+    keep, pp, wp, n0, opt, bx, stream = _prepare(points, weights, box, comm.device, stream, leaf_size, flags,
+                                                 out_host)
+    if points is None:
+        if n is None:
+            raise ValueError("ranks without points must pass n")
+        n0 = int(n)
+        # the device input flag must agree with rank 0's (it only tells rank 0 how to read points)
+    out = ctypes.c_void_p()
+    status = L.pd_build_sharded(comm.ptr, pp, wp, n0, ctypes.byref(bx) if bx is not None else None,
+                                ctypes.byref(opt), ctypes.byref(out))
+    del keep
     _check(status)
     return _wrap(out.value, stream)
 
@@ -306,6 +383,20 @@ def export_slice(d: Diagram, stream=None):
                              rn.data_ptr(), ra.data_ptr(), ctypes.byref(total), ctypes.c_void_p(stream)))
     t = int(total.value)
     return cnt, vol, surf, flg, rn[:t], ra[:t]
+
+
+def measure_fp32_peak(device: int = 0, reps: int = 5) -> float:
+    """pd_measure_fp32_peak: FP32 FFMA lane-ops/s of the device (roofline denominator)."""
+    v = ctypes.c_double()
+    _check(load_library().pd_measure_fp32_peak(int(device), int(reps), ctypes.byref(v)))
+    return v.value
+
+
+def measure_l2_peak(device: int = 0, nbytes: int = 48 << 20, reps: int = 5) -> float:
+    """pd_measure_l2_peak: L2-resident read bytes/s of the device (roofline denominator)."""
+    v = ctypes.c_double()
+    _check(load_library().pd_measure_l2_peak(int(device), int(nbytes), int(reps), ctypes.byref(v)))
+    return v.value
 
 
 def trim(device: int = 0):

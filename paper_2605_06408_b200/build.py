@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)
         objs.append(obj)
-    cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB_OUT + ".tmp"] + objs + ["-lcudart"]
+    cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB_OUT + ".tmp"] + objs + ["-lcudart", "-ldl"]
     subprocess.check_call(cmd)
     os.replace(LIB_OUT + ".tmp", LIB_OUT)
     return LIB_OUT

@@ -15,6 +15,7 @@
 
 #include "../../include/pd.h"
 #include "pd_bvh.cuh"
+#include "pd_comm.cuh"
 #include "pd_internal.cuh"
 
 struct pd_result {
@@ -240,15 +241,40 @@ void finish_outputs(pd_result* r, Arena& A, unsigned flags, cudaStream_t st) {
     (void)A;
 }
 
+void nck(ncclResult_t r, const char* where) {
+    if (r != ncclSuccess) {
+        pd::nccl_set_error(where, r);
+        throw Fail{PD_ENCCL};
+    }
+}
+
+// Header rank 0 broadcasts before the arrays of a sharded build (pd_build_sharded).
+struct ShardHeader {
+    int64_t status, err_index, n, n_wide;
+    float box[6];
+    int32_t has_box, pad;
+};
+
+// comm == nullptr: pd_build (whole diagram, or the opt.shard_rank slice without an exchange).
+// comm != nullptr: pd_build_sharded -- rank 0 packs, validates and builds the LBVH, NCCL broadcasts the
+// sorted sites, the permutation and the wide nodes; every rank builds its Morton slice of the cells; the
+// slices are exchanged (grouped NCCL broadcasts) and every rank assembles the full CSR.
 pd_status build_impl(const float* points, const float* weights, int64_t n, const pd_box* box, const pd_options* optp,
-                     pd_result** out) {
+                     pd_result** out, pd_comm* comm = nullptr) {
     pd_options opt;
     memset(&opt, 0, sizeof(opt));
     if (optp) opt = *optp;
     if (!out) return PD_EINVAL;
     *out = nullptr;
+    const bool root_builds = !comm || comm->rank == 0;  // this rank packs the input and builds the LBVH
+    if (comm) {
+        opt.device = comm->device;
+        opt.shard_world = comm->world;
+        opt.shard_rank = comm->rank;
+        if (opt.flags & PD_TETS) return PD_EINVAL;
+    }
     if (n == 0) return PD_EEMPTY;
-    if (n < 0 || n > PD_MAX_SITES || !points) return PD_EINVAL;
+    if (n < 0 || n > PD_MAX_SITES || (root_builds && !points)) return PD_EINVAL;
     if (box)
         for (int k = 0; k < 3; ++k)
             if (!(box->lo[k] < box->hi[k]) || !std::isfinite(box->lo[k]) || !std::isfinite(box->hi[k])) return PD_EINVAL;
@@ -276,6 +302,15 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         Ev ev[5];
         for (auto& e : ev) e.create();
         ck(cudaEventRecord(ev[0], st));
+        float4* sorted = nullptr;
+        int32_t* perm = nullptr;
+        int* bvh_counters = nullptr;  // collapse counters ([1] = capacity overflow), checked after the cells
+        pd::Bvh bvh;
+        float hbox[6] = {0, 0, 0, 0, 0, 0};
+        int64_t n_wide = 0;
+        pd_status root_status = PD_OK;
+        int64_t root_err = -1;
+        if (root_builds) {
         // ---- inputs
         const float* dpts = points;
         const float* dw = weights;
@@ -306,12 +341,13 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         }
         ck(pd::bvh_pack(dpts, dw, n, box, sites, box_dev, errs, aabb, st, &launches));
         unsigned long long herr[2];
-        float hbox[6];
         ck(cudaMemcpyAsync(herr, errs, sizeof(herr), cudaMemcpyDeviceToHost, st));
         ck(cudaMemcpyAsync(hbox, box_dev, sizeof(hbox), cudaMemcpyDeviceToHost, st));
         ck(cudaStreamSynchronize(st));
-        if (herr[0] != ~0ull) { g_err_index = (int64_t)herr[0]; throw Fail{PD_ENONFINITE}; }
-        if (herr[1] != ~0ull) { g_err_index = (int64_t)herr[1]; throw Fail{PD_EOUTSIDE}; }
+        if (herr[0] != ~0ull) { root_err = (int64_t)herr[0]; root_status = PD_ENONFINITE; }
+        else if (herr[1] != ~0ull) { root_err = (int64_t)herr[1]; root_status = PD_EOUTSIDE; }
+        if (root_status != PD_OK && !comm) { g_err_index = root_err; throw Fail{root_status}; }
+        if (root_status == PD_OK) {
         // a degenerate tight box (all points on a plane) is widened so cells stay 3-D
         if (!box) {
             bool changed = false;
@@ -333,8 +369,8 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         ck(pd::sort_pairs(keys, keys_s, vals, vals_s, n, nullptr, &tb, st, nullptr));
         void* tmp = W.alloc<unsigned char>(tb);
         ck(pd::sort_pairs(keys, keys_s, vals, vals_s, n, tmp, &tb, st, &launches));
-        float4* sorted = W.alloc<float4>(n);
-        int32_t* perm = A.alloc<int32_t>(n);
+        sorted = W.alloc<float4>(n);
+        perm = A.alloc<int32_t>(n);
         ck(pd::bvh_gather(sites, vals_s, n, sorted, perm, st, &launches));
         // ---- a6/a7 LBVH + refit
         pd::BvhScratch sc;
@@ -346,7 +382,6 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         sc.visit = W.alloc<int>(ni);
         sc.blo = W.alloc<float4>(ni);
         sc.bhi = W.alloc<float4>(ni);
-        pd::Bvh bvh;
         sc.max_wide = (int)std::min<int64_t>(2 * n / leaf + 2, ni + 1);
         bvh.nodes = W.alloc<pd::WideNode>(sc.max_wide);
         sc.tasks[0] = W.alloc<int2>(sc.max_wide);
@@ -354,6 +389,51 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         sc.counters = W.alloc<int>(pd::kCollapseCounters);
         bvh.root = W.alloc<pd::NodeChild>(1);
         ck(pd::bvh_topology(keys_s, sorted, (int)n, leaf, sc, bvh, st, &launches));
+        bvh_counters = sc.counters;
+        if (comm && n > leaf) {  // the wide-node count sizes the broadcast
+            int hc[2] = {0, 0};
+            ck(cudaMemcpyAsync(hc, sc.counters, sizeof(hc), cudaMemcpyDeviceToHost, st));
+            ck(cudaStreamSynchronize(st));
+            if (hc[1]) throw Fail{PD_EINTERNAL};  // collapse capacity invariant violated
+            n_wide = hc[0];
+        }
+        }  // root_status == PD_OK
+        }  // root_builds
+        if (comm) {
+            // ---- broadcast the header (status first: every rank returns rank 0's input error), then the
+            // LBVH: Morton-sorted sites, the permutation and the wide nodes + root record (NCCL over NVLink)
+            const pd::NcclApi* nc = pd::nccl_api();
+            if (!nc) throw Fail{PD_ENCCL};
+            ShardHeader* dh = W.alloc<ShardHeader>(1);
+            ShardHeader hh;
+            memset(&hh, 0, sizeof(hh));
+            if (root_builds) {
+                hh.status = root_status; hh.err_index = root_err; hh.n = n; hh.n_wide = n_wide;
+                for (int k = 0; k < 6; ++k) hh.box[k] = hbox[k];
+                ck(cudaMemcpyAsync(dh, &hh, sizeof(hh), cudaMemcpyHostToDevice, st));
+            }
+            nck(nc->Broadcast(dh, dh, sizeof(hh), ncclUint8, 0, comm->comm, st), "ncclBroadcast(header)");
+            ck(cudaMemcpyAsync(&hh, dh, sizeof(hh), cudaMemcpyDeviceToHost, st));
+            ck(cudaStreamSynchronize(st));
+            if (hh.status != PD_OK) { g_err_index = hh.err_index; throw Fail{(pd_status)hh.status}; }
+            if (hh.n != n) throw Fail{PD_EINVAL};  // every rank must pass the same n
+            n_wide = hh.n_wide;
+            for (int k = 0; k < 6; ++k) hbox[k] = hh.box[k];
+            if (!root_builds) {
+                sorted = W.alloc<float4>(n);
+                perm = A.alloc<int32_t>(n);
+                bvh.nodes = W.alloc<pd::WideNode>(std::max<int64_t>(n_wide, 1));
+                bvh.root = W.alloc<pd::NodeChild>(1);
+            }
+            nck(nc->GroupStart(), "ncclGroupStart");
+            nck(nc->Broadcast(sorted, sorted, (size_t)n * 4, ncclFloat32, 0, comm->comm, st), "ncclBroadcast(sites)");
+            nck(nc->Broadcast(perm, perm, (size_t)n, ncclInt32, 0, comm->comm, st), "ncclBroadcast(perm)");
+            if (n_wide > 0)
+                nck(nc->Broadcast(bvh.nodes, bvh.nodes, (size_t)n_wide * sizeof(pd::WideNode), ncclUint8, 0, comm->comm, st),
+                    "ncclBroadcast(nodes)");
+            nck(nc->Broadcast(bvh.root, bvh.root, sizeof(pd::NodeChild), ncclUint8, 0, comm->comm, st), "ncclBroadcast(root)");
+            nck(nc->GroupEnd(), "ncclGroupEnd");
+        }
         ck(cudaEventRecord(ev[1], st));
         // ---- cells
         int32_t* cnt = A.alloc<int32_t>(n);
@@ -376,7 +456,8 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         // PD_BALANCE cuts equal estimated cost, from the tier-1 kernel's per-cell work counters on a
         // strided ~40k-cell sample (deterministic, so every rank computes the same cuts).  Measured on
         // C4 at world 8 (tools/shard_balance.py): equal-count max/mean 1.07, cost-balanced 1.16.
-        int64_t begin = (n * rank) / world, end = (n * (rank + 1)) / world;
+        std::vector<int64_t> cuts(world + 1);  // every rank's slice (the exchange needs them all)
+        for (int q = 0; q <= world; ++q) cuts[q] = (n * q) / world;
         if (world > 1 && (opt.flags & PD_BALANCE) && n >= 4 * world) {
             const int64_t stride = std::max<int64_t>(1, n / 40000);
             const int64_t ns = (n + stride - 1) / stride;
@@ -437,9 +518,9 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
                 int64_t k = std::lower_bound(cum.begin(), cum.end(), target) - cum.begin();
                 return std::min<int64_t>(n, std::max<int64_t>(0, (k - 1) * stride));
             };
-            begin = cut(rank);
-            end = cut(rank + 1);
+            for (int q = 0; q <= world; ++q) cuts[q] = cut(q);
         }
+        const int64_t begin = cuts[rank], end = cuts[rank + 1];
         r->slice_begin = begin;
         r->slice_end = end;
         // ---- optional KNN warm start: K = 8 nearest sites of every site of the slice
@@ -567,24 +648,29 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             int ovf = 0, t_ovf = 0;
             ck(cudaMemcpyAsync(&top, counters + 4, sizeof(top), cudaMemcpyDeviceToHost, st));
             ck(cudaMemcpyAsync(&ovf, aovf, sizeof(ovf), cudaMemcpyDeviceToHost, st));
+            int collapse_ovf = 0;
+            if (bvh_counters) ck(cudaMemcpyAsync(&collapse_ovf, bvh_counters + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
             if (want_tets) {
                 ck(cudaMemcpyAsync(&ttop, counters + 5, sizeof(ttop), cudaMemcpyDeviceToHost, st));
                 ck(cudaMemcpyAsync(&t_ovf, tovf, sizeof(t_ovf), cudaMemcpyDeviceToHost, st));
             }
             ck(cudaStreamSynchronize(st));
+            if (collapse_ovf) throw Fail{PD_EINTERNAL};  // LBVH collapse capacity invariant violated (pd_bvh.cu)
             if (!ovf && !t_ovf) break;
             if (attempt == 2) throw Fail{PD_EINTERNAL};
             if (ovf) cap = (int64_t)(top * 1.1) + 1024;  // rerun with an arena large enough
             if (t_ovf) tcap = (int64_t)(ttop * 1.1) + 1024;
         }
         ck(cudaEventRecord(ev[2], st));
+        int64_t nnz = 0;
+        int64_t* offsets = nullptr;
+        if (!comm) {
         // ---- a13 CSR
-        int64_t* offsets = A.alloc<int64_t>((size_t)n + 1);
+        offsets = A.alloc<int64_t>((size_t)n + 1);
         size_t sb = 0;
         ck(pd::scan_counts(cnt, offsets, n, nullptr, &sb, st, nullptr));
         void* stmp = W.alloc<unsigned char>(sb);
         ck(pd::scan_counts(cnt, offsets, n, stmp, &sb, st, &launches));
-        int64_t nnz = 0;
         ck(cudaMemcpyAsync(&nnz, offsets + n, sizeof(nnz), cudaMemcpyDeviceToHost, st));
         ck(cudaStreamSynchronize(st));
         if (nnz > cap) throw Fail{PD_EINTERNAL};
@@ -603,6 +689,74 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             r->ntets = nt;
             r->tets = (int32_t*)to_result(r, A, tt);
         }
+        } else {
+            // ---- exchange: this rank's slice in Morton order goes straight into
+            // the full Morton-ordered arrays at its offset; the row counts are all-gathered; every block is
+            // then broadcast by its owner (grouped NCCL broadcasts = an all-gather of variable-size blocks);
+            // every rank assembles the full original-order CSR.
+            const pd::NcclApi* nc = pd::nccl_api();
+            const int64_t len = end - begin;
+            int32_t* cnt_m = W.alloc<int32_t>(n);
+            float* vol_m = W.alloc<float>(n);
+            float* surf_m = W.alloc<float>(n);
+            uint8_t* flags_m = W.alloc<uint8_t>(n);
+            int64_t* moff = W.alloc<int64_t>((size_t)len + 1);
+            ck(pd::slice_export_meta(perm, begin, len, cnt, vol, surf, flags, cnt_m + begin, vol_m + begin,
+                                     surf_m + begin, flags_m + begin, st, &launches));
+            size_t sb = 0;
+            ck(pd::scan_counts(cnt_m + begin, moff, len, nullptr, &sb, st, nullptr));
+            ck(pd::scan_counts(cnt_m + begin, moff, len, W.alloc<unsigned char>(sb), &sb, st, &launches));
+            int64_t* rows_all = W.alloc<int64_t>(world);
+            nck(nc->AllGather(moff + len, rows_all, 1, ncclInt64, comm->comm, st), "ncclAllGather(rows)");
+            std::vector<int64_t> hrows(world), roff(world + 1, 0);
+            ck(cudaMemcpyAsync(hrows.data(), rows_all, sizeof(int64_t) * world, cudaMemcpyDeviceToHost, st));
+            ck(cudaStreamSynchronize(st));
+            for (int q = 0; q < world; ++q) roff[q + 1] = roff[q] + hrows[q];
+            const int64_t total = roff[world];
+            int32_t* rows_nbr = W.alloc<int32_t>((size_t)std::max<int64_t>(total, 1));
+            float* rows_area = W.alloc<float>((size_t)std::max<int64_t>(total, 1));
+            ck(pd::slice_export_rows(perm, begin, len, cnt_m + begin, moff, aoff, anbr, aarea, rows_nbr + roff[rank],
+                                     rows_area + roff[rank], st, &launches));
+            nck(nc->GroupStart(), "ncclGroupStart");
+            for (int q = 0; q < world; ++q) {
+                const int64_t b = cuts[q], lq = cuts[q + 1] - cuts[q];
+                if (lq > 0) {
+                    nck(nc->Broadcast(cnt_m + b, cnt_m + b, (size_t)lq, ncclInt32, q, comm->comm, st), "ncclBroadcast(cnt)");
+                    nck(nc->Broadcast(vol_m + b, vol_m + b, (size_t)lq, ncclFloat32, q, comm->comm, st), "ncclBroadcast(vol)");
+                    nck(nc->Broadcast(surf_m + b, surf_m + b, (size_t)lq, ncclFloat32, q, comm->comm, st), "ncclBroadcast(surf)");
+                    nck(nc->Broadcast(flags_m + b, flags_m + b, (size_t)lq, ncclUint8, q, comm->comm, st), "ncclBroadcast(flags)");
+                }
+                if (hrows[q] > 0) {
+                    nck(nc->Broadcast(rows_nbr + roff[q], rows_nbr + roff[q], (size_t)hrows[q], ncclInt32, q, comm->comm, st),
+                        "ncclBroadcast(rows)");
+                    nck(nc->Broadcast(rows_area + roff[q], rows_area + roff[q], (size_t)hrows[q], ncclFloat32, q, comm->comm,
+                                      st), "ncclBroadcast(areas)");
+                }
+            }
+            nck(nc->GroupEnd(), "ncclGroupEnd");
+            // ---- assemble the full CSR in original order on every rank (same kernels as pd_assemble)
+            int32_t* cnt_o = A.alloc<int32_t>(n);
+            float* vol_o = A.alloc<float>(n);
+            float* surf_o = A.alloc<float>(n);
+            uint8_t* flags_o = A.alloc<uint8_t>(n);
+            ck(pd::assemble_meta(perm, n, cnt_m, vol_m, surf_m, flags_m, cnt_o, vol_o, surf_o, flags_o, st, &launches));
+            int64_t* moff_all = W.alloc<int64_t>((size_t)n + 1);
+            offsets = A.alloc<int64_t>((size_t)n + 1);
+            size_t sb1 = 0, sb2 = 0;
+            ck(pd::scan_counts(cnt_m, moff_all, n, nullptr, &sb1, st, nullptr));
+            ck(pd::scan_counts(cnt_m, moff_all, n, W.alloc<unsigned char>(sb1), &sb1, st, &launches));
+            ck(pd::scan_counts(cnt_o, offsets, n, nullptr, &sb2, st, nullptr));
+            ck(pd::scan_counts(cnt_o, offsets, n, W.alloc<unsigned char>(sb2), &sb2, st, &launches));
+            nbr = A.alloc<int32_t>((size_t)std::max<int64_t>(total, 1));
+            area = A.alloc<float>((size_t)std::max<int64_t>(total, 1));
+            ck(pd::assemble_rows(perm, n, cnt_m, moff_all, offsets, rows_nbr, rows_area, nbr, area, st, &launches));
+            nnz = total;
+            cnt = cnt_o;
+            vol = vol_o;
+            surf = surf_o;
+            flags = flags_o;
+            r->slice_nnz = hrows[rank];
+        }
         ck(cudaEventRecord(ev[3], st));
         r->nnz = nnz;
         r->offsets = to_result(r, A, offsets);
@@ -614,7 +768,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         r->perm = to_result(r, A, perm);
         r->cnt = to_result(r, A, cnt);
         if (cost) r->cost = to_result(r, A, cost);
-        r->slice_nnz = nnz;
+        if (!comm) r->slice_nnz = nnz;
         finish_outputs(r, A, opt.flags, st);
         ck(cudaEventRecord(ev[4], st));
         pd::Stats hs;
@@ -677,6 +831,20 @@ pd_status pd_build(const float* points, const float* weights, int64_t n, const p
                    pd_result** out) {
     try {
         return build_impl(points, weights, n, box, opt, out);
+    } catch (...) {
+        if (out) *out = nullptr;
+        return PD_EINTERNAL;
+    }
+}
+
+pd_status pd_build_sharded(pd_comm* comm, const float* points, const float* weights, int64_t n, const pd_box* box,
+                           const pd_options* opt, pd_result** out) {
+    if (!comm) {
+        if (out) *out = nullptr;
+        return PD_EINVAL;
+    }
+    try {
+        return build_impl(points, weights, n, box, opt, out, comm);
     } catch (...) {
         if (out) *out = nullptr;
         return PD_EINTERNAL;
@@ -853,6 +1021,7 @@ const char* pd_strerror(pd_status s) {
 }
 int64_t pd_error_index(void) { return g_err_index; }
 const char* pd_last_cuda_error(void) { return g_cuda_msg; }
+const char* pd_last_nccl_error(void) { return pd::nccl_last_error(); }
 int pd_abi_version(void) { return PD_ABI_VERSION; }
 int64_t pd_last_launch_count(void) { return g_launches; }
 

@@ -89,7 +89,10 @@ struct TierCfg {
 };
 
 #ifndef PD_T1_MINB
-#define PD_T1_MINB 5
+#define PD_T1_MINB 20  // resident one-warp CTAs per SM (register cap 96)
+#endif
+#ifndef PD_T1_WARPS
+#define PD_T1_WARPS 1  // one warp per CTA: the warp's state sits at a constant shared-memory address
 #endif
 #ifndef PD_T1_Q
 #define PD_T1_Q 64
@@ -103,7 +106,7 @@ struct TierCfg {
 #ifndef PD_T1_SPHERE
 #define PD_T1_SPHERE 0
 #endif
-using Tier1 = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, 4, PD_T1_MINB, false, false, PD_T1_SPHERE != 0>;
+using Tier1 = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, PD_T1_WARPS, PD_T1_MINB, false, false, PD_T1_SPHERE != 0>;
 // Tier 2: one cell per CTA of 4 warps (state in shared memory, O(V) passes CTA-wide from 128 vertices):
 // the few heavy cells of a light-weight workload (C4: 78) no longer run on one warp each, which
 // mattered most for the per-rank critical path of sharded builds.
@@ -886,15 +889,33 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         int kmin = __reduce_min_sync(FULL, cand ? ford(key) : 0x7fffffff);
         unsigned lead = __ballot_sync(FULL, cand && ford(key) == kmin);
         int src = __ffs(lead) - 1;
+        if (lane == src) cand = false;
+        // Fast reject, lane = vertex: the plane (D, dd) of the leaf's candidate pass, its margin m (from the
+        // leaf-time vmax >= the current one: only larger).  No FP32 value above -m means every vertex is
+        // strictly inside (|s32 - s| < m), which is exactly when the certified classification of clip()
+        // would remove nothing: such a plane never cuts this or any later (smaller) cell.
+        FPlane f;
+        f.nx = __shfl_sync(FULL, Dx, src); f.ny = __shfl_sync(FULL, Dy, src); f.nz = __shfl_sync(FULL, Dz, src);
+        f.d = __shfl_sync(FULL, dd, src);
+        f.m = __shfl_sync(FULL, m, src);
+        {
+            const int nv0 = c.nv;
+            bool maybe = false;
+            for (int sv = lane; sv < nv0; sv += 32) {
+                const float4 v = S.fv[sv];
+                maybe |= fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d > -f.m;
+            }
+            if (!__any_sync(FULL, maybe)) {
+                mask = __ballot_sync(FULL, cand);
+                continue;
+            }
+        }
         float sx = __shfl_sync(FULL, sj.x, src), sy = __shfl_sync(FULL, sj.y, src), sz = __shfl_sync(FULL, sj.z, src),
               sw = __shfl_sync(FULL, sj.w, src);
-        if (lane == src) cand = false;
-        FPlane f;
-        f.nx = sx - c.fpx; f.ny = sy - c.fpy; f.nz = sz - c.fpz;
-        float f2 = f.nx * f.nx + f.ny * f.ny + f.nz * f.nz, fdq = c.fpw - sw;
-        f.d = 0.5f * (f2 + fdq);
-        f.m = 1e-6f * ((fabsf(f.nx) + fabsf(f.ny) + fabsf(f.nz)) * c.vmax + f2 + fabsf(fdq));
-        f.tl = 1e-12f * (f2 * rsqrtf(f2)) * c.rmax;
+        {
+            const float f2 = f.nx * f.nx + f.ny * f.ny + f.nz * f.nz;
+            f.tl = 1e-12f * (f2 * rsqrtf(f2)) * c.rmax;
+        }
         PT_BEGIN(t_clip);
         const int jsrc = __shfl_sync(FULL, j, src);
         int st = clip(S, c, lane, make_float4(sx, sy, sz, sw), f, jsrc, cnt);
@@ -1485,8 +1506,11 @@ __device__ __noinline__ void emit_tets(WarpState<T>& S, const Cell& c, int lane,
 }
 
 // Face areas (vector area 1/2 sum v x next(v) around each face), volume, neighbours; FP64.
+// Returns the cell's robustness counts packed: faces dropped (bits 0-14), near-degenerate neighbour faces
+// (bits 15-29), degraded (bit 30) -- returned rather than added to the caller's Counters, which would
+// otherwise have its address taken by this out-of-line call and live on the thread stack.
 template <class T>
-__device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const CellParams& P, int status, Counters& cnt) {
+__device__ __noinline__ unsigned finalize(WarpState<T>& S, Cell& c, int lane, const CellParams& P, int status) {
     const int i = c.self_orig;
     const CellOut& O = P.out;
     if (status == ST_EMPTY || status == ST_DUP || status == ST_OVERFLOW) {
@@ -1499,7 +1523,7 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
             O.flags[i] = (uint8_t)(status == ST_OVERFLOW ? PD_CELL_OVERFLOW
                                                          : (PD_CELL_EMPTY | (status == ST_DUP ? PD_CELL_DUPLICATE : 0)));
         }
-        return;
+        return 0u;
     }
     double vol = 0, surf = 0;
     if (T::COOP && c.nv >= P_coop_min_v(S)) {  // twins and faces over all warps of the CTA
@@ -1572,9 +1596,6 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
     }
     if (O.tarena) emit_tets(S, c, lane, P, amin);
     const bool degraded = c.degraded != 0;
-    cnt.dropped += ndrop;
-    cnt.small += nsmall;
-    cnt.degraded += degraded ? 1u : 0u;
     if (lane == 0) {
         O.cnt[i] = K;
         O.aoff[i] = base;
@@ -1583,6 +1604,7 @@ __device__ __noinline__ void finalize(WarpState<T>& S, Cell& c, int lane, const 
         O.flags[i] = (uint8_t)((boundary ? PD_CELL_BOUNDARY : 0) | (vol > 0 ? 0 : PD_CELL_EMPTY) |
                                (degraded ? PD_CELL_DEGRADED : 0));
     }
+    return min(ndrop, 0x7fffu) | (min(nsmall, 0x7fffu) << 15) | (degraded ? 1u << 30 : 0u);
 }
 
 __device__ __noinline__ void trace_print(int tier, const Cell& c, const Counters& a, const Counters& b, int st, long long cyc) {
@@ -1600,8 +1622,8 @@ __device__ __noinline__ void trace_print(int tier, const Cell& c, const Counters
 }
 
 template <class T, unsigned MODE>
-__global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(CellParams P, int tier) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+__global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(const __grid_constant__ CellParams P, int tier) {
+    const int lane = threadIdx.x & 31, wid = T::WARPS == 1 ? 0 : (int)(threadIdx.x >> 5);
     WarpState<T>& S = T::COOP     ? (T::GLOBAL ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x]
                                                : *reinterpret_cast<WarpState<T>*>(pd_smem + coop_smem_bytes<T>()))
                       : T::GLOBAL ? reinterpret_cast<WarpState<T>*>(P.gstate)[blockIdx.x * T::WARPS + wid]
@@ -1615,8 +1637,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
         }
     }
     const int64_t total = P.list ? (int64_t)(*P.list_count) : P.count;
-    Counters cnt;
-    memset(&cnt, 0, sizeof(cnt));
+    Counters cnt = {};
     // spill stack per cell program: per warp, or per CTA in a cooperative tier (only warp 0 traverses)
     const int gw = T::COOP ? blockIdx.x : blockIdx.x * T::WARPS + wid;
     NodeChild* spill = P.spill + (size_t)gw * P.spill_cap;
@@ -1670,7 +1691,10 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(Cel
             }
             if (st == ST_OVERFLOW) novf++;
             PT_BEGIN(t_fin);
-            finalize(S, c, lane, P, st, cnt);
+            const unsigned rob = finalize(S, c, lane, P, st);
+            cnt.dropped += rob & 0x7fffu;
+            cnt.small += (rob >> 15) & 0x7fffu;
+            cnt.degraded += rob >> 30;
             PT_END(t_fin, 5);
             ncells++;
 #if PD_PROFILE

@@ -1,9 +1,10 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): the Morton-slice partition and the all-gather
-exchange of variable-length row blocks used by paper_2605_06408_b200.dist.
+"""Multi-rank host logic on CPU (gloo, world_size 2 and 3): the Morton-slice partition and the exchange
+protocol of pd_build_sharded (all-gather of row counts, owner broadcasts of variable-size blocks into the
+full Morton-ordered arrays), modelled by paper_2605_06408_b200.dist.exchange_blocks.
 
-The GPU reassembly kernel (pd_assemble) is checked byte-for-byte against world=1 on the GPU in
-tests/test_gpu_parity.py::test_sharded_reassembly_matches_single; here the exchange is checked
-against a numpy model of the same reassembly, with oracle rows as the per-cell payload.
+The GPU path (NCCL inside libpd) is checked byte-for-byte against pd_build on one GPU with a loopback
+communicator in tests/test_gpu_parity.py::test_build_sharded_loopback; here the protocol is checked
+against a numpy model of the reassembly, with oracle rows as the per-cell payload.
 """
 import os
 import socket
@@ -46,13 +47,13 @@ def _worker(rank, world, port, payload, q):
         ridx = np.concatenate(rows) if rows else np.zeros(0, np.int64)
         blk = (torch.from_numpy(c.astype(np.int32)), torch.from_numpy(vol[ids]), torch.from_numpy(surf[ids]),
                torch.from_numpy(flags[ids]), torch.from_numpy(nbr[ridx]), torch.from_numpy(area[ridx]))
-        full = exchange_blocks(blk)
+        full = exchange_blocks(blk, n)
         q.put((rank, [t.numpy() for t in full]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_exchange_blocks_gloo(world):
     wl = pdgen.make("C3", n=1500)
     o = oracle.cells(wl.points, wl.weights, wl.box)

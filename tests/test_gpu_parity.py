@@ -365,6 +365,34 @@ def test_sharded_reassembly_matches_single():
             assert np.array_equal(getattr(ref, k), getattr(full, k)), (world, k)
 
 
+def test_build_sharded_loopback():
+    """pd_build_sharded through a real NCCL communicator of one rank (the only GPU of the test box): the
+    header + LBVH broadcasts, the slice export, the owner broadcasts and the assembly run, and the result is
+    byte-identical to pd_build.  Host and device inputs; rank 0's input errors are
+    returned with their index."""
+    wl = pdgen.make("C5", n=40009)
+    ref = _gpu(wl)
+    comm = pd.Comm(pd.Comm.unique_id(), 0, 1, 0)
+    try:
+        p = torch.from_numpy(wl.points).cuda()
+        w = torch.from_numpy(wl.weights).cuda()
+        for d in (pd.build_sharded(comm, p, w, wl.box).to_numpy(),
+                  pd.build_sharded(comm, wl.points, wl.weights, wl.box, out_host=True),
+                  pd.build_sharded(comm, p, w, wl.box, flags=pd.BALANCE).to_numpy()):
+            for k in ("offsets", "neighbors", "areas", "volumes", "surface", "flags"):
+                assert np.array_equal(getattr(ref, k), getattr(d, k)), k
+        bad = wl.points.copy()
+        bad[123, 2] = np.inf
+        with pytest.raises(pd.PdError) as e:
+            pd.build_sharded(comm, bad, wl.weights, wl.box)
+        assert e.value.status == pd.PD_ENONFINITE and e.value.index == 123
+        with pytest.raises(pd.PdError) as e:
+            pd.build_sharded(comm, wl.points, wl.weights, wl.box, flags=pd.TETS)
+        assert e.value.status == pd.PD_EINVAL
+    finally:
+        comm.close()
+
+
 @pytest.mark.parametrize("n,bits", [(1, 62), (1000, 8), (4096 * 3 + 17, 62), (1_000_003, 62), (2_000_000, 20)])
 def test_own_radix_sort_matches_stable_torch_sort(n, bits):
     """a4: the path's own LSD radix sort equals a stable sort (ties keep input order)."""
