@@ -8,7 +8,8 @@ synthetic workload, inputs resident in HBM (value), and the same through the C A
 buffers + host outputs (e2e).  At N=1 the workload is C4 (10M scene-like power diagram,
 BASELINE.json configs[3], the config the metric is quoted on).  For N>1 (torchrun, one rank per GPU)
 the cells are split into Morton slices (strong scaling: the 10M diagram is fixed), exchanged with
-NCCL all-gathers and reassembled on every rank; time = max over ranks.
+NCCL inside libpd (pd_build_sharded: rank-0 input, LBVH broadcast, owner broadcasts of the slices, assembly
+on every rank); time = max over ranks.
 
 `--impl reference` times the CPU oracle (oracle/, the reference arm of this tier) on host cores on a
 bounded sample of the same workload's cells per step; under torchrun only rank 0 runs it.
@@ -32,7 +33,8 @@ METRIC = "Mcells/s for 10M-point power diagram"
 UNIT = "Mcells/s"
 # Algorithmic FP work per cell (SURVEY.md §8(d) "Algorithmic work per cell": W_min ≈ 25·300 node
 # tests + 15·450 site tests + 4·27·77 vertex classifications + 40·27 vertex creations ≈ 2.3e4
-# FP ops/cell).  Peak = 148 SMs × 128 FP32 lanes × 1.965 GHz (B200_PROFILING.md nominal units).
+# FP ops/cell).  The peak is MEASURED in the same job (pd_measure_fp32_peak); the nominal
+# 148 SMs × 128 FP32 lanes × 1.965 GHz is reported beside it.
 W_MIN_OPS_PER_CELL = 2.3e4
 ALU_PEAK_TOPS = 148 * 128 * 1.965e9 / 1e12
 
@@ -118,13 +120,20 @@ def cpu_baseline(wl, budget_s: float = 15.0, seed: int = 7):
                       f"{dt:.1f} s wall on {threads} threads"}
 
 
-def profile_traffic():
-    """DRAM bytes per launch of the cell kernel from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "cells_kernel_traffic.json")
-    try:
-        return json.load(open(p))
-    except Exception:
-        return None
+def profile_metrics():
+    """ncu counters of the tier-1 cell kernel (C4, 10M sites) from this round's capture, committed under
+    profiles/ by tools/profile_round.sh: DRAM bytes per launch (roofline.traffic), FP32 lane-ops, L2 bytes,
+    issue / occupancy / divergence.  ncu cannot run inside the timed bench; the file names its capture."""
+    for name in ("r2_cells_metrics.json", "cells_kernel_traffic.json"):
+        p = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(p):
+            try:
+                d = json.load(open(p))
+                d["_file"] = "profiles/" + name
+                return d
+            except Exception:
+                pass
+    return None
 
 
 def run_reference(args):
@@ -174,28 +183,39 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     pd.load_library()
-    wl, gen_s = load_workload(args.config, args.n)
     dev = torch.device("cuda", local)
-    p = torch.from_numpy(wl.points).to(dev)
-    w = None if wl.weights is None else torch.from_numpy(wl.weights).to(dev)
+    # the workload lives on rank 0 (points start on rank 0); the others learn n
+    wl, gen_s = (load_workload(args.config, args.n) if rank == 0 else (None, 0.0))
+    n = wl.n if rank == 0 else 0
+    if world > 1:
+        obj = [n]
+        dist.broadcast_object_list(obj, src=0)
+        n = obj[0]
+    p = torch.from_numpy(wl.points).to(dev) if rank == 0 else None
+    w = (None if wl.weights is None else torch.from_numpy(wl.weights).to(dev)) if rank == 0 else None
+    box = wl.box if rank == 0 else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
     stream = torch.cuda.current_stream(dev)
+    comm = pddist.init_comm(device=local) if world > 1 else None
 
     base_flags = pd.WARM_START if args.warm_start else (pd.WARM_ADAPTIVE if args.warm_adaptive else 0)
 
-    def step(flags=0):
+    def step(flags=0, host=False):
         flags |= base_flags
-        if world > 1:
-            return pddist.build_diagram_distributed(p, w, wl.box, leaf_size=args.leaf, flags=flags)
-        return pd.build_diagram(p, w, wl.box, leaf_size=args.leaf, flags=flags)
+        pts, wts = (p, w) if not host else (hp.numpy() if rank == 0 else None,
+                                           (None if hw is None else hw.numpy()) if rank == 0 else None)
+        if world > 1:  # pd_build_sharded: rank-0 input, NCCL broadcast of the LBVH, slice, exchange, assemble
+            return pd.build_sharded(comm, pts, wts, box, n=n, leaf_size=args.leaf, flags=flags, out_host=host)
+        return pd.build_diagram(pts, wts, box, leaf_size=args.leaf, flags=flags, out_host=host)
 
+    hp = torch.from_numpy(wl.points).pin_memory() if rank == 0 else None
+    hw = (None if wl.weights is None else torch.from_numpy(wl.weights).pin_memory()) if rank == 0 else None
     for _ in range(args.warmup):
         d = step()
         del d
     torch.cuda.synchronize()
-    # stats pass (counters), not timed
-    d = pd.build_diagram(p, w, wl.box, leaf_size=args.leaf, flags=pd.STATS | base_flags, shard_rank=rank,
-                         shard_world=world)
+    # stats pass (counters of this rank's slice), not timed
+    d = step(pd.STATS)
     stats = dict(d.stats)
     nnz_total = int(d.nnz)
     flags_np = d.flags.cpu().numpy()
@@ -216,8 +236,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         launches += pd.last_launch_count()
         step_ms.append(e0.elapsed_time(e1))
-        if world == 1:
-            cell_ms.append(d.stats["ms_cells"])
+        cell_ms.append(d.stats["ms_cells"])
         del d
     clocks = sampler.stop()
     ms = float(np.mean(step_ms))
@@ -225,63 +244,82 @@ def run_ours(args):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = wl.n / (ms / 1e3) / 1e6
+    value = n / (ms / 1e3) / 1e6
 
-    # ---- e2e through the C ABI with pinned host buffers and host outputs
-    hp = torch.from_numpy(wl.points).pin_memory()
-    hw = None if wl.weights is None else torch.from_numpy(wl.weights).pin_memory()
+    # ---- e2e through the C ABI: pinned host input (rank 0), host outputs (every rank), copies timed
     e2e_ms = []
-    h2d = hp.numel() * 4 + (0 if hw is None else hw.numel() * 4)
+    h2d = (hp.numel() * 4 + (0 if hw is None else hw.numel() * 4)) if rank == 0 else 0
     d2h = 0
     for it in range(1 + args.steps):
         flush.fill_(1.0)
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        pts = hp.numpy()
-        d = pd.build_diagram(pts, None if hw is None else hw.numpy(), wl.box, leaf_size=args.leaf, out_host=True,
-                             flags=base_flags, shard_rank=rank, shard_world=world)
+        d = step(host=True)
         dt = time.perf_counter() - t0
         d2h = (d.n + 1) * 8 + d.nnz * 8 + d.n * 9
         del d
         if it > 0:
             e2e_ms.append(dt * 1e3)
-    e2e_v = wl.n / (float(np.mean(e2e_ms)) / 1e3) / 1e6
+    e2e_t = float(np.mean(e2e_ms))
     if world > 1:
-        t = torch.tensor([e2e_v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        e2e_v = float(t.item())
+        t = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    e2e_v = n / (e2e_t / 1e3) / 1e6
+
+    # ---- roofline denominators measured on this box, in this job
+    fp32_peak = pd.measure_fp32_peak(local) / 1e12   # T lane-ops/s (FFMA chains)
+    l2_peak = pd.measure_l2_peak(local) / 1e9        # GB/s (L2-resident reads)
 
     line = None
     if rank == 0:
         cells_rank = stats["cells"]
-        kms = float(np.mean(cell_ms)) if cell_ms else stats["ms_cells"]
+        kms = float(np.mean(cell_ms))
         achieved = W_MIN_OPS_PER_CELL * cells_rank / (kms / 1e3) / 1e12
-        traffic = profile_traffic()
-        roof = {"bound": "alu", "achieved": achieved, "peak": ALU_PEAK_TOPS, "unit": "TFLOP/s",
-                "frac": achieved / ALU_PEAK_TOPS,
-                "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+        met = profile_metrics()
+        roof = {"bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak,
+                "traffic": met.get("dram_bytes_per_launch") if met else None,
                 "kernel": "cells_kernel (3 capacity tiers, one launch each)",
                 "kernel_ms": kms, "kernel_share_of_step": kms / ms if world == 1 else None,
-                "work_model": "W_min = 2.3e4 FP ops/cell (SURVEY.md §8(d)); peak = 148 SM x 128 lanes x 1.965 GHz "
-                              "(derived, not measured; MEASURED_PEAKS.json has no FP32 figure)"}
-        if traffic:  # what actually bounds it (ncu, tier-1 launch on C4): instruction issue, not FP32 or DRAM
-            roof["ncu_issue_slot_util"] = traffic.get("issue_active_pct", 0) / 100.0
-            roof["ncu_warps_active"] = traffic.get("warps_active_pct", 0) / 100.0
-            roof["ncu_dram_gbs"] = traffic["dram_bytes_per_launch"] / traffic["duration_ns"]
-            roof["ncu_warp_inst_per_cell"] = traffic["inst_executed"] / 1e7
+                "work_model": "achieved = W_min 2.3e4 FP32 lane-ops/cell (SURVEY.md §8(d)) x cells of this rank / "
+                              "cell-kernel time (CUDA events on the launching stream); peak = FFMA-chain "
+                              "microbenchmark on this GPU in this job (pd_measure_fp32_peak)",
+                "fp32_peak_measured": fp32_peak, "fp32_peak_nominal": ALU_PEAK_TOPS,
+                "l2_peak_measured": l2_peak, "frac_useful": achieved / fp32_peak}
+        if met:  # what the counters say (ncu capture of the same code, profiles/)
+            dur_s = met["duration_ns"] * 1e-9
+            if "fp32_lane_ops" in met:
+                roof["frac_fp32_pipe"] = met["fp32_lane_ops"] / dur_s / 1e12 / fp32_peak
+            if "lts_bytes" in met:
+                roof["frac_l2"] = met["lts_bytes"] / dur_s / 1e9 / l2_peak
+            roof["ncu_issue_slot_util"] = met.get("issue_active_pct", 0) / 100.0
+            roof["ncu_warps_active"] = met.get("warps_active_pct", 0) / 100.0
+            if "threads_per_inst" in met:
+                roof["ncu_divergence"] = met["threads_per_inst"] / 32.0
+            if "ipc" in met:
+                roof["ncu_ipc"] = met["ipc"]
+            roof["ncu_dram_gbs"] = met["dram_bytes_per_launch"] / met["duration_ns"]
+            roof["ncu_warp_inst_per_cell"] = met["inst_executed"] / met.get("cells", 1e7)
+            roof["ncu_source"] = met["_file"]
+        cfg = {"workload": f"{wl.name}: {wl.description}", "n": n, "box": list(wl.box),
+               "leaf_size": args.leaf or 32, "parallelism": f"seed-sharded x{world}",
+               "warm_start": "all" if args.warm_start else ("adaptive" if args.warm_adaptive else "off"),
+               "l2": "flushed before every timed step (256 MiB write)", "generation_s": round(gen_s, 1)}
+        if world > 1:
+            cfg["input"] = "points on rank 0; LBVH NCCL-broadcast, slices exchanged (pd_build_sharded)"
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic",
-                "config": {"workload": f"{wl.name}: {wl.description}", "n": wl.n, "box": list(wl.box),
-                           "leaf_size": args.leaf or 32, "parallelism": f"seed-sharded x{world}",
-                           "warm_start": "all" if args.warm_start else ("adaptive" if args.warm_adaptive else "off"),
-                           "l2": "flushed before every timed step (256 MiB write)", "generation_s": round(gen_s, 1)},
+                "vs_baseline": None, "dtype": "f64+f32", "data": "synthetic", "config": cfg,
                 "roofline": roof,
                 "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
                 "clocks": clocks, "gpu_launches": int(launches),
                 "stats": {k: stats[k] for k in ("nodes_visited", "leaves_visited", "sites_tested", "clip_tests",
                                                  "clips", "tier_cells", "overflow_cells", "ms_bvh", "ms_cells",
-                                                 "ms_csr", "ms_tier", "ms_knn")},
+                                                 "ms_csr", "ms_tier", "ms_knn", "faces_dropped",
+                                                 "faces_near_degenerate", "degraded_cells")},
                 "nnz": nnz_total, "empty_ratio": float(np.mean(flags_np & 1)),
                 "step_ms": [round(x, 3) for x in step_ms]}
         if world == 1 and not args.no_cpu_baseline:
@@ -289,6 +327,7 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+        comm.close()
         dist.destroy_process_group()
     return 0
 
