@@ -105,25 +105,28 @@ def load_library(path: str | None = None):
     L.pd_last_cuda_error.restype = ctypes.c_char_p
     L.pd_abi_version.restype = ctypes.c_int
     L.pd_last_launch_count.restype = I64
-    L.pd_trim.restype = ctypes.c_int
-    L.pd_trim.argtypes = [ctypes.c_int]
-    L.pd_comm_unique_id.restype = ctypes.c_int
-    L.pd_comm_unique_id.argtypes = [P]
-    L.pd_comm_init.restype = ctypes.c_int
-    L.pd_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P)]
-    L.pd_build_sharded.restype = ctypes.c_int
-    L.pd_build_sharded.argtypes = [P, P, P, I64, P, P, ctypes.POINTER(P)]
-    L.pd_comm_free.restype = None
-    L.pd_comm_free.argtypes = [P]
-    L.pd_comm_rank.restype = ctypes.c_int
-    L.pd_comm_rank.argtypes = [P]
-    L.pd_comm_world.restype = ctypes.c_int
-    L.pd_comm_world.argtypes = [P]
-    L.pd_last_nccl_error.restype = ctypes.c_char_p
-    L.pd_measure_fp32_peak.restype = ctypes.c_int
-    L.pd_measure_fp32_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
-    L.pd_measure_l2_peak.restype = ctypes.c_int
-    L.pd_measure_l2_peak.argtypes = [ctypes.c_int, I64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    if hasattr(L, "pd_trim"):  # (older A/B builds of the library lack the newer entry points)
+        L.pd_trim.restype = ctypes.c_int
+        L.pd_trim.argtypes = [ctypes.c_int]
+    if hasattr(L, "pd_build_sharded"):
+        L.pd_comm_unique_id.restype = ctypes.c_int
+        L.pd_comm_unique_id.argtypes = [P]
+        L.pd_comm_init.restype = ctypes.c_int
+        L.pd_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(P)]
+        L.pd_build_sharded.restype = ctypes.c_int
+        L.pd_build_sharded.argtypes = [P, P, P, I64, P, P, ctypes.POINTER(P)]
+        L.pd_comm_free.restype = None
+        L.pd_comm_free.argtypes = [P]
+        L.pd_comm_rank.restype = ctypes.c_int
+        L.pd_comm_rank.argtypes = [P]
+        L.pd_comm_world.restype = ctypes.c_int
+        L.pd_comm_world.argtypes = [P]
+        L.pd_last_nccl_error.restype = ctypes.c_char_p
+    if hasattr(L, "pd_measure_fp32_peak"):
+        L.pd_measure_fp32_peak.restype = ctypes.c_int
+        L.pd_measure_fp32_peak.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+        L.pd_measure_l2_peak.restype = ctypes.c_int
+        L.pd_measure_l2_peak.argtypes = [ctypes.c_int, I64, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     if hasattr(L, "pd_tets"):
         L.pd_num_tets.restype = I64
         L.pd_num_tets.argtypes = [P]

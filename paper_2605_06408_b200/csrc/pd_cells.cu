@@ -67,6 +67,12 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PD_EDGE_BITMAP
 #define PD_EDGE_BITMAP 0
 #endif
+#ifndef PD_FAST_REJECT
+#define PD_FAST_REJECT 0  // per candidate, FP32-only "can this plane cut at all" pass (superseded by the pre-test)
+#endif
+#ifndef PD_PRETEST
+#define PD_PRETEST 1  // per leaf: every candidate against every vertex at once (lane = vertex), FP32 only
+#endif
 
 template <int V, int P, int Q, int W, int MINB, bool GLOB = false, bool CO = false, bool SPH = false>
 struct TierCfg {
@@ -89,10 +95,10 @@ struct TierCfg {
 };
 
 #ifndef PD_T1_MINB
-#define PD_T1_MINB 20  // resident one-warp CTAs per SM (register cap 96)
+#define PD_T1_MINB 5  // resident CTAs per SM (register cap 96)
 #endif
 #ifndef PD_T1_WARPS
-#define PD_T1_WARPS 1  // one warp per CTA: the warp's state sits at a constant shared-memory address
+#define PD_T1_WARPS 4  // 1: one-warp CTAs (constant smem address) measured 9% lower issue efficiency on C4
 #endif
 #ifndef PD_T1_Q
 #define PD_T1_Q 64
@@ -169,6 +175,8 @@ struct __align__(16) WarpState {
     uint32_t qmask[T::QC];        // alive-entry ballots of the current pop
     uint32_t bnd[T::VMAX];        // boundary edges (x | y << 16) of the current clip (B <= VMAX unless overflow)
     uint16_t pmap[T::PMAX];       // plane GC remap
+    float4 cpl[32];               // a leaf's candidates, lane = candidate: FP32 plane (D = p_j - p_i, dd = q/2)
+    __align__(16) float cmg[32];  //   and its certification margin (kept in smem, not registers, through clip())
     uint32_t ebits[T::EBW];       // hole-edge parity bitmap (zero between clips)
 };
 
@@ -236,8 +244,10 @@ constexpr unsigned kModeBits = PD_ISOTROPIC | PD_DFS | PD_PAPER_BOUND | PD_EXACT
 constexpr unsigned kDynMode = 0xffffffffu;
 template <unsigned MODE>
 __device__ __forceinline__ unsigned mode_flags(unsigned runtime_flags) {
-    return MODE == kDynMode ? runtime_flags : (MODE | (runtime_flags & ~kModeBits));
+    return MODE == kDynMode ? runtime_flags : ((MODE & kModeBits) | (runtime_flags & ~kModeBits));
 }
+template <unsigned MODE>
+constexpr bool kStats = MODE == kDynMode || (MODE & PD_STATS) != 0;  // u64 pd_stats counters compiled in
 
 // Exact node tests switch on once a cell has visited `after` nodes (heavy cells), or always with
 // PD_EXACT_NODES; PD_NO_EXACT disables them.
@@ -252,9 +262,13 @@ enum { CLIP_NONE = 0, CLIP_DONE = 1, CLIP_EMPTY = 2, CLIP_OVF = 3 };
 #ifndef PD_PROFILE
 #define PD_PROFILE 0
 #endif
+// Work counters.  The u64 totals (pd_stats) are compiled in only for kernels instantiated with PD_STATS (or the
+// generic-mode kernels of the higher tiers): in the default tier-1 kernel they would hold ~12 registers across
+// the whole cell program.  `work` (nodes + sites + 8 clips of the current cell: PD_COST, the longest-first
+// order of the next tier) and `visited` (nodes of the current cell: the exact-test switch) are always kept.
 struct Counters {
     unsigned long long nodes, leaves, sites, tests, clips, spills;
-    unsigned dropped, small, degraded;  // robustness counters (always published)
+    unsigned work, visited;             // per cell
 #if PD_PROFILE
     unsigned long long cyc[10];  // init, descend, leaf, clip, pop, finalize | clip: classify, boundary, create, aabb
 #endif
@@ -533,15 +547,26 @@ __device__ __noinline__ void plane_gc(WarpState<T>& S, Cell& c, int lane) {
     __syncwarp();
 }
 
-__device__ __forceinline__ void solve3(double4 a, double4 b, double4 c, double& x, double& y, double& z) {
-    double bcx = b.y * c.z - b.z * c.y, bcy = b.z * c.x - b.x * c.z, bcz = b.x * c.y - b.y * c.x;
-    double cax = c.y * a.z - c.z * a.y, cay = c.z * a.x - c.x * a.z, caz = c.x * a.y - c.y * a.x;
-    double abx = a.y * b.z - a.z * b.y, aby = a.z * b.x - a.x * b.z, abz = a.x * b.y - a.y * b.x;
-    double det = a.x * bcx + a.y * bcy + a.z * bcz;
-    double inv = 1.0 / det;
-    x = (a.w * bcx + b.w * cax + c.w * abx) * inv;
-    y = (a.w * bcy + b.w * cay + c.w * aby) * inv;
-    z = (a.w * bcz + b.w * caz + c.w * abz) * inv;
+// Vertex of three planes n.y = d (Cramer's rule), staged so that only one cross product is live at a time
+// (register pressure of the inlined hot loop): x = (a.w (b x c) + b.w (c x a) + c.w (a x b)) / (a . (b x c)).
+__device__ __forceinline__ void solve3(const double4* pl, int ia, int ib, int ic, double& x, double& y, double& z) {
+    const double4 b = pl[ib], c = pl[ic];
+    double det;
+    {
+        const double bcx = b.y * c.z - b.z * c.y, bcy = b.z * c.x - b.x * c.z, bcz = b.x * c.y - b.y * c.x;
+        const double4 a = pl[ia];
+        det = a.x * bcx + a.y * bcy + a.z * bcz;
+        x = a.w * bcx; y = a.w * bcy; z = a.w * bcz;
+    }
+    {
+        const double4 a = pl[ia];
+        const double cax = c.y * a.z - c.z * a.y, cay = c.z * a.x - c.x * a.z, caz = c.x * a.y - c.y * a.x;
+        x += b.w * cax; y += b.w * cay; z += b.w * caz;
+        const double abx = a.y * b.z - a.z * b.y, aby = a.z * b.x - a.x * b.z, abz = a.x * b.y - a.y * b.x;
+        x += c.w * abx; y += c.w * aby; z += c.w * abz;
+    }
+    const double inv = 1.0 / det;
+    x *= inv; y *= inv; z *= inv;
 }
 
 // Clip the cell by {y : n.y <= d} (re-designed warp-parallel).
@@ -622,7 +647,6 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
     if (R == nv0) return CLIP_EMPTY;
     __syncwarp();
     PT_BEGIN(t_bnd);
-    const double4 pl = exact_plane(c, sj);
     int np0 = c.np;
     if (np0 >= (T::PMAX * 85) / 100) {  // plane garbage collection (vertex slots are unaffected)
         plane_gc(S, c, lane);
@@ -731,8 +755,8 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
     if (nvn > T::VMAX || B > T::VMAX || np0 + 1 > T::PMAX) return CLIP_OVF;
     // 3. append the plane, create (h, x, y) for every boundary edge
     int hs = np0;
-    if (lane == 0) {
-        S.pl[hs] = pl;
+    if (lane == 0) {  // the exact FP64 plane goes straight to shared memory (read back by every new vertex)
+        S.pl[hs] = exact_plane(c, sj);
         S.pid[hs] = pidn;
     }
     __syncwarp();
@@ -742,7 +766,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
             uint32_t be = S.bnd[e];
             int x = be & 0xffff, y = be >> 16;
             double vx, vy, vz;
-            solve3(pl, S.pl[x], S.pl[y], vx, vy, vz);
+            solve3(S.pl, hs, x, y, vx, vy, vz);
             int slot = e < R ? S.rem[e] : nv0 + (e - R);
             put_vertex(S.fv, S.vx, S.vy, S.vz, slot, vx, vy, vz);
             S.vt[slot] = tpack<typename T::trip_t>(hs, x, y);
@@ -785,9 +809,8 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
 // SPHERE tiers also bound the support by the cell's bounding sphere, h <= m.D + rho |D|: much tighter
 // than the box for the huge, round cells of heavy sites, whose AABB holds thousands of candidates.
 template <bool SPH>
-__device__ __forceinline__ bool site_culled(const Cell& c, float Dx, float Dy, float Dz, float D2, float dq,
-                                            unsigned flags) {
-    const float q = D2 + dq;
+__device__ __forceinline__ bool site_culled_hq(const Cell& c, float Dx, float Dy, float Dz, float D2, float hq, float dqa,
+                                               unsigned flags) {
     if (!(flags & (PD_PAPER_BOUND | PD_ISOTROPIC))) {
         float h = Dx * (Dx >= 0.f ? c.fhi[0] : c.flo[0]) + Dy * (Dy >= 0.f ? c.fhi[1] : c.flo[1]) +
                   Dz * (Dz >= 0.f ? c.fhi[2] : c.flo[2]);
@@ -797,7 +820,7 @@ __device__ __forceinline__ bool site_culled(const Cell& c, float Dx, float Dy, f
             h = fminf(h, fmaf(c.sc[0], Dx, fmaf(c.sc[1], Dy, c.sc[2] * Dz)) + rd);
             mag += rd;
         }
-        return 0.5f * q - h > 1e-5f * (D2 + fabsf(dq) + mag);
+        return hq - h > 1e-5f * (D2 + dqa + mag);
     }
     float r2;
     if (flags & PD_ISOTROPIC) {
@@ -807,7 +830,18 @@ __device__ __forceinline__ bool site_culled(const Cell& c, float Dx, float Dy, f
         r2 = hx * hx + hy * hy + hz * hz;
     }
     float rd = sqrtf(r2 * D2);
-    return q - 2.f * rd > 1e-5f * (D2 + fabsf(dq) + 2.f * rd);
+    return 2.f * hq - 2.f * rd > 1e-5f * (D2 + dqa + 2.f * rd);
+}
+template <bool SPH>
+__device__ __forceinline__ bool site_culled(const Cell& c, float Dx, float Dy, float Dz, float D2, float dq,
+                                            unsigned flags) {
+    return site_culled_hq<SPH>(c, Dx, Dy, Dz, D2, 0.5f * (D2 + dq), fabsf(dq), flags);
+}
+// Re-cull from a candidate's stored plane (D, dd = q/2): |dq| = |2 dd - D2| only sizes the relative margin.
+template <bool SPH>
+__device__ __forceinline__ bool site_culled_pl(const Cell& c, float4 pl, unsigned flags) {
+    const float D2 = pl.x * pl.x + pl.y * pl.y + pl.z * pl.z;
+    return site_culled_hq<SPH>(c, pl.x, pl.y, pl.z, D2, pl.w, fabsf(2.f * pl.w - D2), flags);
 }
 
 // FP64 certification of a candidate whose FP32 cut test was ambiguous (rare; kept out of line).
@@ -842,7 +876,8 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         }
     }
     if (__any_sync(FULL, dup_kill)) return ST_DUP;
-    cnt.sites += count;
+    if (kStats<MODE>) cnt.sites += count;
+    cnt.work += count;
     bool cand = valid && !site_culled<T::SPHERE>(c, Dx, Dy, Dz, D2, dq, flags);
     unsigned mask = __ballot_sync(FULL, cand);
     if (!mask) return ST_OK;
@@ -863,7 +898,7 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
             }
             if (!cuts && amb) cuts = cuts_fp64(S, c, sj, D2);  // certify in FP64 (rare)
         }
-        cnt.tests += __popc(mask);
+        if (kStats<MODE>) cnt.tests += __popc(mask);
         cand = cand && cuts;
         mask = __ballot_sync(FULL, cand);
     }
@@ -878,13 +913,43 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         unsigned cut = 0u;
         for (int w = 0; w < T::WARPS; ++w) cut |= (unsigned)J.ipart[w][0];
         const bool cuts = (cut >> lane) & 1u;
-        cnt.tests += __popc(mask);
+        if (kStats<MODE>) cnt.tests += __popc(mask);
         cand = cand && cuts;
         mask = __ballot_sync(FULL, cand);
         batched = true;
     }
-    if (!batched) cnt.tests += __popc(mask);
+    if (!batched && kStats<MODE>) cnt.tests += __popc(mask);
     float key = cand ? dd * rsqrtf(D2) : INFINITY;  // d_ij: nearest plane first
+    // the candidates' planes wait in shared memory (lane = candidate), so that no per-candidate value but
+    // the key stays in registers through clip()
+    if (cand) { S.cpl[lane] = make_float4(Dx, Dy, Dz, dd); S.cmg[lane] = m; }
+    __syncwarp();
+    if (PD_PRETEST && !batched) {
+        // Pre-test, lane = vertex, all candidates at once (independent FMA chains, groups of 4 planes in
+        // flight): bit k <=> candidate k has some FP32 value above -m_k on the CURRENT cell.  A candidate
+        // with none has every vertex strictly inside (|s32 - s| < m), i.e. the certified classification
+        // of clip() would remove nothing now or on any later (smaller) cell: dropped for good.
+        unsigned hit = 0u;
+        const int nv0 = c.nv;
+        for (int sv = lane; sv - lane < nv0; sv += 32) {
+            const bool vin = sv < nv0;
+            const float4 v = vin ? S.fv[sv] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+            for (int k0 = 0; k0 < 32; k0 += 4) {
+                const unsigned g = (mask >> k0) & 0xfu;
+                if (!g) continue;
+                const float4 mg = *reinterpret_cast<const float4*>(&S.cmg[k0]);
+                const float4 p0 = S.cpl[k0], p1 = S.cpl[k0 + 1], p2 = S.cpl[k0 + 2], p3 = S.cpl[k0 + 3];
+                const bool h0 = fmaf(p0.x, v.x, fmaf(p0.y, v.y, p0.z * v.z)) - p0.w > -mg.x;
+                const bool h1 = fmaf(p1.x, v.x, fmaf(p1.y, v.y, p1.z * v.z)) - p1.w > -mg.y;
+                const bool h2 = fmaf(p2.x, v.x, fmaf(p2.y, v.y, p2.z * v.z)) - p2.w > -mg.z;
+                const bool h3 = fmaf(p3.x, v.x, fmaf(p3.y, v.y, p3.z * v.z)) - p3.w > -mg.w;
+                if (vin) hit |= ((h0 ? 1u : 0u) | (h1 ? 2u : 0u) | (h2 ? 4u : 0u) | (h3 ? 8u : 0u)) << k0;
+            }
+        }
+        mask &= __reduce_or_sync(FULL, hit);
+        cand = (mask >> lane) & 1u;
+    }
     while (mask) {
         int kmin = __reduce_min_sync(FULL, cand ? ford(key) : 0x7fffffff);
         unsigned lead = __ballot_sync(FULL, cand && ford(key) == kmin);
@@ -895,10 +960,12 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         // strictly inside (|s32 - s| < m), which is exactly when the certified classification of clip()
         // would remove nothing: such a plane never cuts this or any later (smaller) cell.
         FPlane f;
-        f.nx = __shfl_sync(FULL, Dx, src); f.ny = __shfl_sync(FULL, Dy, src); f.nz = __shfl_sync(FULL, Dz, src);
-        f.d = __shfl_sync(FULL, dd, src);
-        f.m = __shfl_sync(FULL, m, src);
         {
+            const float4 pl = S.cpl[src];
+            f.nx = pl.x; f.ny = pl.y; f.nz = pl.z; f.d = pl.w;
+            f.m = S.cmg[src];
+        }
+        if (PD_FAST_REJECT) {
             const int nv0 = c.nv;
             bool maybe = false;
             for (int sv = lane; sv < nv0; sv += 32) {
@@ -910,21 +977,21 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
                 continue;
             }
         }
-        float sx = __shfl_sync(FULL, sj.x, src), sy = __shfl_sync(FULL, sj.y, src), sz = __shfl_sync(FULL, sj.z, src),
-              sw = __shfl_sync(FULL, sj.w, src);
+        const int jsrc = __shfl_sync(FULL, j, src);
+        const float4 sjs = __ldg(&P.sites[jsrc]);  // the site itself (FP64 plane of the certification)
         {
             const float f2 = f.nx * f.nx + f.ny * f.ny + f.nz * f.nz;
             f.tl = 1e-12f * (f2 * rsqrtf(f2)) * c.rmax;
         }
         PT_BEGIN(t_clip);
-        const int jsrc = __shfl_sync(FULL, j, src);
-        int st = clip(S, c, lane, make_float4(sx, sy, sz, sw), f, jsrc, cnt);
+        int st = clip(S, c, lane, sjs, f, jsrc, cnt);
         PT_END(t_clip, 3);
         if (st == CLIP_EMPTY) return ST_EMPTY;
         if (st == CLIP_OVF) return ST_OVERFLOW;
         if (st == CLIP_DONE) {
-            cnt.clips++;
-            if (cand && site_culled<T::SPHERE>(c, Dx, Dy, Dz, D2, dq, flags)) cand = false;
+            if (kStats<MODE>) cnt.clips++;
+            cnt.work += 8;
+            if (cand && site_culled_pl<T::SPHERE>(c, S.cpl[lane], flags)) cand = false;
         }
         mask = __ballot_sync(FULL, cand);
     }
@@ -984,13 +1051,14 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
     bool warm = (mode_flags<MODE>(P.flags) & PD_WARM_START) && P.knn;
     const int root_link = node;
     int ns = 0;  // spilled entries
-    const unsigned long long nodes0 = cnt.nodes;
     int nq = 0;  // queue length (warp-uniform register)
     for (;;) {
         if (have) {
             PT_BEGIN(t_desc);
             while (node >= 0 && !warm) {  // descend (Alg. 1 lines 4-18), 8 children per visit
-                cnt.nodes++;
+                if (kStats<MODE>) cnt.nodes++;
+                cnt.work++;
+                cnt.visited++;
                 float key = INFINITY;
                 bool culled = true;
                 float4 lo_w = make_float4(0, 0, 0, 0), hi_l = make_float4(0, 0, 0, 0);
@@ -1001,7 +1069,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     if (__float_as_int(hi_l.w) != EMPTY_LINK) key = node_test(c, lo_w, hi_l, flags, culled);
                 }
                 unsigned surv = __ballot_sync(FULL, !culled);
-                const bool ex_all = exact_on(flags, cnt.nodes - nodes0, P.exact_after);
+                const bool ex_all = exact_on(flags, cnt.visited, P.exact_after);
                 // exact test on every surviving LEAF child (a leaf costs far more than the test), and on
                 // internal children too once the cell is heavy
                 const unsigned leafm = __ballot_sync(FULL, lane < WIDE && __float_as_int(hi_l.w) < 0);
@@ -1058,13 +1126,13 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     }
                     nq += npush - tos;
                     ns += tos;
-                    cnt.spills += tos;
+                    if (kStats<MODE>) cnt.spills += tos;
                 }
                 node = lnear;
             }
             if (have) {
                 PT_END(t_desc, 1);
-                cnt.leaves++;
+                if (kStats<MODE>) cnt.leaves++;
                 __syncwarp();
                 PT_BEGIN(t_leaf);
                 int st = process_leaf<T, MODE>(S, c, lane, node, warm, P, cnt);
@@ -1136,7 +1204,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             __syncwarp();
             bool culled;
             node_test(c, lo, hi, flags, culled);
-            if (!culled && (exact_on(flags, cnt.nodes - nodes0, P.exact_after) ||
+            if (!culled && (exact_on(flags, cnt.visited, P.exact_after) ||
                             (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) && __float_as_int(hi.w) < 0)))
                 culled = node_exact_culled(S, c, lane, lo, hi);
             node = __float_as_int(hi.w);
@@ -1181,7 +1249,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         unsigned lead = __ballot_sync(FULL, bestk == gk);
         int bslot = __shfl_sync(FULL, bests, __ffs(lead) - 1);
         node = __float_as_int(qhi[bslot].w);
-        bool popped_dead = (exact_on(flags, cnt.nodes - nodes0, P.exact_after) ||
+        bool popped_dead = (exact_on(flags, cnt.visited, P.exact_after) ||
                             (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) && node < 0)) &&
                            node_exact_culled(S, c, lane, qlo[bslot], qhi[bslot]);
         if (PD_LAZY_COMPACT && alive_total < 0) {  // warp path: alive count from the chunk ballots
@@ -1663,7 +1731,11 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(con
                 continue;
             }
             Cell& c = S.c;
+#if PD_PROFILE
             const Counters before = cnt;
+#endif
+            cnt.work = 0;
+            cnt.visited = 0;
             float4 site = __ldg(&P.sites[s]);
             c.fpx = site.x; c.fpy = site.y; c.fpz = site.z; c.fpw = site.w;
             c.px = site.x; c.py = site.y; c.pz = site.z; c.pw = site.w;
@@ -1682,27 +1754,26 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(con
                     int k = atom_add_g32(P.next_count, 1);
                     P.next_list[k] = s;
                     if (P.next_cost) {  // the host starts the next tier's costliest cells first
-                        unsigned long long w = (cnt.nodes - before.nodes) + (cnt.sites - before.sites) +
-                                               8 * (cnt.clips - before.clips);
-                        P.next_cost[k] = (int32_t)min(w, 0x7fffffffull);
+                        P.next_cost[k] = (int32_t)min(cnt.work, 0x7fffffffu);
                     }
                 }
                 continue;
             }
-            if (st == ST_OVERFLOW) novf++;
+            if (kStats<MODE> && st == ST_OVERFLOW) novf++;
             PT_BEGIN(t_fin);
             const unsigned rob = finalize(S, c, lane, P, st);
-            cnt.dropped += rob & 0x7fffu;
-            cnt.small += (rob >> 15) & 0x7fffu;
-            cnt.degraded += rob >> 30;
+            if (rob && lane == 0) {  // robustness counters (rare, always published): straight to the device totals
+                red_add_g(&P.stats->dropped, rob & 0x7fffu);
+                red_add_g(&P.stats->small, (rob >> 15) & 0x7fffu);
+                red_add_g(&P.stats->degraded, rob >> 30);
+            }
             PT_END(t_fin, 5);
-            ncells++;
+            if (kStats<MODE>) ncells++;
 #if PD_PROFILE
             if (c.self_orig == P.trace_cell && lane == 0) trace_print(tier, c, cnt, before, st, clock64() - t_cell);
 #endif
             if ((P.flags & PD_COST) && lane == 0) {  // deterministic work count (balanced cuts must agree)
-                unsigned long long w = (cnt.nodes - before.nodes) + (cnt.sites - before.sites) + 8 * (cnt.clips - before.clips);
-                P.out.cost[c.self_orig] = (int32_t)min(w, 0x7fffffffull);
+                P.out.cost[c.self_orig] = (int32_t)min(cnt.work, 0x7fffffffu);
             }
             __syncwarp();
         }
@@ -1713,7 +1784,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(con
         named_bar(1, T::WARPS * 32);
     }
     // counters of every tier, or only of tier $PD_PROF_TIER when it is set (per-tier profiles)
-    if ((P.flags & PD_STATS) && lane == 0 && (P.prof_tier < 0 || P.prof_tier == tier)) {
+    if (kStats<MODE> && (P.flags & PD_STATS) && lane == 0 && (P.prof_tier < 0 || P.prof_tier == tier)) {
         red_add_g(&P.stats->nodes, cnt.nodes);
         red_add_g(&P.stats->leaves, cnt.leaves);
         red_add_g(&P.stats->sites, cnt.sites);
@@ -1727,11 +1798,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(con
         for (int k = 0; k < 10; ++k) red_add_g(&P.stats->cyc[k], cnt.cyc[k]);
 #endif
     }
-    if (lane == 0 && (cnt.dropped | cnt.small | cnt.degraded)) {  // robustness counters: always
-        red_add_g(&P.stats->dropped, cnt.dropped);
-        red_add_g(&P.stats->small, cnt.small);
-        red_add_g(&P.stats->degraded, cnt.degraded);
-    }
+
 }
 
 template <class T, unsigned MODE>
@@ -1762,12 +1829,19 @@ cudaError_t launch_tier(const CellParams& p, int tier, cudaStream_t st, int num_
 cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches) {
     if (launches) ++*launches;
     if (tier == 0) {
-        switch (p.flags & kModeBits) {  // tier 1: specialized kernels for the common modes
+        // tier 1: specialized kernels for the common modes, each with and without the pd_stats counters
+        constexpr unsigned S = PD_STATS;
+        switch (p.flags & (kModeBits | PD_STATS)) {
             case 0: return launch_tier<Tier1, 0u>(p, 0, st, num_sms);
+            case S: return launch_tier<Tier1, S>(p, 0, st, num_sms);
             case PD_PAPER_BOUND: return launch_tier<Tier1, PD_PAPER_BOUND>(p, 0, st, num_sms);
+            case PD_PAPER_BOUND | S: return launch_tier<Tier1, PD_PAPER_BOUND | S>(p, 0, st, num_sms);
             case PD_ISOTROPIC: return launch_tier<Tier1, PD_ISOTROPIC>(p, 0, st, num_sms);
+            case PD_ISOTROPIC | S: return launch_tier<Tier1, PD_ISOTROPIC | S>(p, 0, st, num_sms);
             case PD_DFS: return launch_tier<Tier1, PD_DFS>(p, 0, st, num_sms);
+            case PD_DFS | S: return launch_tier<Tier1, PD_DFS | S>(p, 0, st, num_sms);
             case PD_WARM_START: return launch_tier<Tier1, PD_WARM_START>(p, 0, st, num_sms);
+            case PD_WARM_START | S: return launch_tier<Tier1, PD_WARM_START | S>(p, 0, st, num_sms);
             default: return launch_tier<Tier1, kDynMode>(p, 0, st, num_sms);
         }
     }
@@ -1783,6 +1857,7 @@ int cells_grid_warps(int tier, int num_sms) {
     // all tier-1 instantiations share one register/smem footprint bound; take the largest grid
     if (tier == 0) {
         int g = tier_grid<Tier1, 0u>(num_sms);
+        g = max(g, tier_grid<Tier1, PD_STATS>(num_sms));
         g = max(g, tier_grid<Tier1, PD_PAPER_BOUND>(num_sms));
         g = max(g, tier_grid<Tier1, PD_ISOTROPIC>(num_sms));
         g = max(g, tier_grid<Tier1, PD_DFS>(num_sms));
