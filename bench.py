@@ -120,6 +120,27 @@ def cpu_baseline(wl, budget_s: float = 15.0, seed: int = 7):
                       f"{dt:.1f} s wall on {threads} threads"}
 
 
+def cpu_reference(wl, budget_s: float = 10.0, seed: int = 8):
+    """the CPU reference of the same definition (oracle/pd_oracle.c orc_run_kdtree: the
+    oracle's clipper fed by a k-d tree in ascending distance, stopped by the radius of security), all host
+    threads, on a bounded random sample of the workload's cells.  Reported beside the oracle baseline."""
+    import oracle
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(seed)
+    probe = rng.choice(wl.n, size=min(wl.n, 64 * threads), replace=False)
+    t = time.time()
+    oracle.cells(wl.points, wl.weights, wl.box, ids=probe, threads=threads, kdtree=True)
+    dt = max(time.time() - t, 1e-6)
+    m = int(min(wl.n, max(len(probe), len(probe) * budget_s / dt)))
+    ids = rng.choice(wl.n, size=m, replace=False)
+    t = time.time()
+    oracle.cells(wl.points, wl.weights, wl.box, ids=ids, threads=threads, kdtree=True)
+    dt = time.time() - t
+    return {"value": m / dt / 1e6, "unit": UNIT, "cores": threads, "kind": "kd-tree + security radius (same definition)",
+            "sample": f"{m} random cells of {wl.name} ({wl.n} sites), {dt:.1f} s wall on {threads} threads "
+                      f"(k-d tree build included)"}
+
+
 def profile_metrics():
     """ncu counters of the tier-1 cell kernel (C4, 10M sites) from this round's capture, committed under
     profiles/ by tools/profile_round.sh: DRAM bytes per launch (roofline.traffic), FP32 lane-ops, L2 bytes,
@@ -324,6 +345,7 @@ def run_ours(args):
                 "step_ms": [round(x, 3) for x in step_ms]}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(wl)
+            line["cpu_reference"] = cpu_reference(wl)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -52,6 +52,8 @@ def lib():
         L.orc_nnz.argtypes = [P]
         L.orc_copy.restype = None
         L.orc_copy.argtypes = [P, P, P, P, P, P, P]
+        L.orc_run_kdtree.restype = P
+        L.orc_run_kdtree.argtypes = [P, P, ctypes.c_int64, P, P, ctypes.c_int64, ctypes.c_int]
         L.orc_counts.restype = None
         L.orc_counts.argtypes = [P, P, P]
         L.orc_free.restype = None
@@ -91,14 +93,21 @@ def _prep(points, weights, box):
     return pts, w, bx
 
 
-def cells(points, weights, box, ids=None, threads: int | None = None, order_k: int = 64) -> OracleCells:
-    """Oracle cells for `ids` (default: all).  box = (lo.x, lo.y, lo.z, hi.x, hi.y, hi.z)."""
+def cells(points, weights, box, ids=None, threads: int | None = None, order_k: int = 64,
+          kdtree: bool = False) -> OracleCells:
+    """Oracle cells for `ids` (default: all).  box = (lo.x, lo.y, lo.z, hi.x, hi.y, hi.z).
+    kdtree=True: the CPU reference of the same definition instead (pd_oracle.c orc_run_kdtree: the same
+    clipper, candidates in ascending distance from a k-d tree, stopped by the radius of security) -- a
+    reported CPU baseline; the parity tests use the brute-force oracle."""
     pts, w, bx = _prep(points, weights, box)
     n = pts.shape[0]
     ids = np.arange(n, dtype=np.int64) if ids is None else np.ascontiguousarray(np.asarray(ids, dtype=np.int64))
     threads = threads or os.cpu_count() or 1
     L = lib()
-    r = L.orc_run(_ptr(pts), _ptr(w), n, _ptr(bx), _ptr(ids), len(ids), int(threads), int(order_k))
+    if kdtree:
+        r = L.orc_run_kdtree(_ptr(pts), _ptr(w), n, _ptr(bx), _ptr(ids), len(ids), int(threads))
+    else:
+        r = L.orc_run(_ptr(pts), _ptr(w), n, _ptr(bx), _ptr(ids), len(ids), int(threads), int(order_k))
     try:
         nnz = L.orc_nnz(r)
         m = len(ids)

@@ -519,3 +519,205 @@ int orc_cell_geometry(const float* pts, const float* w, int64_t n, const double*
     ws_free(&ws);
     return nf;
 }
+
+/* ==============================================================================================
+ * CPU reference of the same definition (a reported baseline, NOT the oracle the
+ * parity tests use): the oracle's clipper above, fed candidates in ascending distance from a k-d tree and
+ * stopped by the radius of security (the exact early reject of build_cell turned into a termination test,
+ * the prior-work idea PAPER.md:126, :221): with c = w_i - w_max, the plane of every site at distance
+ * >= D lies at distance >= (D^2 + c)/(2D) from p_i, which is increasing in D once D^2 >= max(0, c); so once
+ * that bound reaches R_max(1+1e-12), no further candidate can cut (same implication as build_cell's skip).
+ * The polytope is the same set as the oracle's (exact arithmetic: clip order is irrelevant); rounding
+ * differs, so tests compare it with the comparator's tolerances.  Multithreaded over cells.
+ * ============================================================================================== */
+
+typedef struct {
+    const orc_input* in;
+    int32_t* idx;      /* permutation of 0..n-1, kd-ordered */
+    int32_t* axis;     /* per implicit node (mid index): split axis */
+    double wmax;
+} kd_tree;
+
+static double coord(const orc_input* in, int32_t j, int ax) { return (double)in->pts[3 * (int64_t)j + ax]; }
+
+static void kd_build_rec(kd_tree* t, int64_t b, int64_t e) {
+    if (e - b <= 1) return;
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    for (int64_t k = b; k < e; ++k)
+        for (int a = 0; a < 3; ++a) {
+            double v = coord(t->in, t->idx[k], a);
+            if (v < lo[a]) lo[a] = v;
+            if (v > hi[a]) hi[a] = v;
+        }
+    int ax = 0;
+    for (int a = 1; a < 3; ++a) if (hi[a] - lo[a] > hi[ax] - lo[ax]) ax = a;
+    int64_t mid = (b + e) / 2;
+    /* quickselect the median on axis ax (ties broken by index: deterministic) */
+    int64_t l = b, r = e - 1;
+    while (l < r) {
+        int32_t piv = t->idx[(l + r) / 2];
+        double pv = coord(t->in, piv, ax);
+        int64_t i = l, j = r;
+        while (i <= j) {
+            while (coord(t->in, t->idx[i], ax) < pv || (coord(t->in, t->idx[i], ax) == pv && t->idx[i] < piv)) ++i;
+            while (coord(t->in, t->idx[j], ax) > pv || (coord(t->in, t->idx[j], ax) == pv && t->idx[j] > piv)) --j;
+            if (i <= j) { int32_t s = t->idx[i]; t->idx[i] = t->idx[j]; t->idx[j] = s; ++i; --j; }
+        }
+        if (mid <= j) r = j; else if (mid >= i) l = i; else break;
+    }
+    t->axis[mid] = ax;
+    kd_build_rec(t, b, mid);
+    kd_build_rec(t, mid + 1, e);
+}
+
+typedef struct { kn_t* h; int n, k; } knn_heap;   /* max-heap on (key, j) of the k best */
+
+static int kn_less(const kn_t* a, const kn_t* b) { return a->key < b->key || (a->key == b->key && a->j < b->j); }
+static void kh_push(knn_heap* H, double key, int64_t j) {
+    kn_t x = {key, j};
+    if (H->n < H->k) {
+        int i = H->n++;
+        while (i > 0) { int p = (i - 1) / 2; if (!kn_less(&H->h[p], &x)) break; H->h[i] = H->h[p]; i = p; }
+        H->h[i] = x;
+    } else if (kn_less(&x, &H->h[0])) {
+        int i = 0;
+        for (;;) {
+            int l = 2 * i + 1, r = l + 1, m = -1;
+            kn_t* best = &x;
+            if (l < H->n && kn_less(best, &H->h[l])) { best = &H->h[l]; m = l; }
+            if (r < H->n && kn_less(best, &H->h[r])) { best = &H->h[r]; m = r; }
+            if (m < 0) break;
+            H->h[i] = H->h[m]; i = m;
+        }
+        H->h[i] = x;
+    }
+}
+
+static void kd_knn_rec(const kd_tree* t, int64_t b, int64_t e, v3 q, knn_heap* H) {
+    if (e <= b) return;
+    int64_t mid = (b + e) / 2;
+    int32_t j = t->idx[mid];
+    v3 pj = site(t->in, j);
+    v3 d = v3sub(pj, q);
+    kh_push(H, v3dot(d, d), j);
+    if (e - b == 1) return;
+    int ax = t->axis[mid];
+    double diff = (ax == 0 ? q.x : ax == 1 ? q.y : q.z) - coord(t->in, j, ax);
+    int64_t nb = diff < 0 ? b : mid + 1, ne = diff < 0 ? mid : e;
+    int64_t fb = diff < 0 ? mid + 1 : b, fe = diff < 0 ? e : mid;
+    kd_knn_rec(t, nb, ne, q, H);
+    if (H->n < H->k || diff * diff <= H->h[0].key) kd_knn_rec(t, fb, fe, q, H);
+}
+
+typedef struct {
+    const orc_input* in;
+    const kd_tree* tree;
+    const int64_t* ids;
+    int64_t ncells;
+    orc_cell* out;
+    int64_t next;
+    pthread_mutex_t mu;
+} kd_job;
+
+static int build_cell_kd(const orc_input* in, const kd_tree* tree, int64_t i, orc_ws* ws, kn_t** buf, int* bufcap,
+                         int* flags) {
+    v3 pi = site(in, i);
+    double wi = wt(in, i);
+    int cur = 0, degraded = 0;
+    *flags = 0;
+    poly_init_box(&ws->P[cur], in->box, pi);
+    double rmax2 = poly_rmax2(&ws->P[cur]);
+    const double c = wi - tree->wmax;
+    int64_t k = 64, pos = 0;
+    for (;;) {
+        int64_t kq = k + 1 < in->n ? k + 1 : in->n;
+        if (*bufcap < kq) { *bufcap = (int)kq; *buf = (kn_t*)realloc(*buf, sizeof(kn_t) * kq); }
+        knn_heap H = {*buf, 0, (int)kq};
+        kd_knn_rec(tree, 0, in->n, pi, &H);
+        qsort(H.h, H.n, sizeof(kn_t), kn_cmp);
+        int stop = 0;
+        for (int64_t t = pos; t < H.n && !stop; ++t) {
+            int64_t j = H.h[t].j;
+            if (j == i) continue;
+            v3 D = v3sub(site(in, j), pi);
+            double D2 = v3dot(D, D);
+            double wj = wt(in, j);
+            if (D2 == 0.0) {
+                if (wj > wi || (wj == wi && j < i)) { *flags |= ORC_EMPTY | ORC_DUPLICATE; return -1; }
+                continue;
+            }
+            double nD = sqrt(D2), rmax = sqrt(rmax2);
+            /* radius of security: every later candidate (distance >= nD) is beyond the cell */
+            if ((c <= 0 || D2 >= c) && (D2 + c) / (2 * nD) >= rmax * (1.0 + 1e-12)) { stop = 1; break; }
+            double dd = 0.5 * (D2 + wi - wj);
+            double dij = dd / nD;
+            if (dij >= rmax * (1.0 + 1e-12)) continue;   /* the oracle's exact skip */
+            double tau = 1e-13 * nD * rmax;
+            int r = poly_clip(&ws->P[cur], &ws->P[cur ^ 1], D, dd, (int)j, tau,
+                              &ws->segs, &ws->segcap, &ws->scratch, &ws->scap, &degraded);
+            if (r == 0) continue;
+            cur ^= 1;
+            if (r == 2) { *flags |= ORC_EMPTY; if (degraded) *flags |= ORC_DEGRADED; return -1; }
+            rmax2 = poly_rmax2(&ws->P[cur]);
+        }
+        if (stop || H.n >= in->n) break;
+        pos = H.n;
+        k *= 4;
+    }
+    if (degraded) *flags |= ORC_DEGRADED;
+    return cur;
+}
+
+static void* kd_worker(void* arg) {
+    kd_job* job = (kd_job*)arg;
+    orc_ws ws;
+    memset(&ws, 0, sizeof(ws));
+    kn_t* buf = NULL;
+    int bufcap = 0;
+    for (;;) {
+        pthread_mutex_lock(&job->mu);
+        int64_t t0 = job->next;
+        job->next += 64;
+        pthread_mutex_unlock(&job->mu);
+        if (t0 >= job->ncells) break;
+        int64_t t1 = t0 + 64 < job->ncells ? t0 + 64 : job->ncells;
+        for (int64_t t = t0; t < t1; ++t) {
+            int flags = 0;
+            int r = build_cell_kd(job->in, job->tree, job->ids[t], &ws, &buf, &bufcap, &flags);
+            finalize_cell(r >= 0 ? &ws.P[r] : NULL, &job->out[t], flags);
+        }
+    }
+    free(buf);
+    ws_free(&ws);
+    return NULL;
+}
+
+/* Same outputs as orc_run (read with orc_nnz / orc_copy / orc_counts / orc_free). */
+orc_result* orc_run_kdtree(const float* pts, const float* w, int64_t n, const double* box, const int64_t* ids,
+                           int64_t ncells, int nthreads) {
+    orc_input in;
+    in.pts = pts; in.w = w; in.n = n; in.order_k = 0;
+    memcpy(in.box, box, sizeof(in.box));
+    kd_tree tree;
+    tree.in = &in;
+    tree.idx = (int32_t*)malloc(sizeof(int32_t) * (n > 0 ? n : 1));
+    tree.axis = (int32_t*)calloc(n > 0 ? n : 1, sizeof(int32_t));
+    tree.wmax = -1e300;
+    for (int64_t j = 0; j < n; ++j) { tree.idx[j] = (int32_t)j; if (wt(&in, j) > tree.wmax) tree.wmax = wt(&in, j); }
+    kd_build_rec(&tree, 0, n);
+    orc_result* res = (orc_result*)calloc(1, sizeof(orc_result));
+    res->ncells = ncells;
+    res->cells = (orc_cell*)calloc(ncells > 0 ? ncells : 1, sizeof(orc_cell));
+    kd_job job;
+    job.in = &in; job.tree = &tree; job.ids = ids; job.ncells = ncells; job.out = res->cells; job.next = 0;
+    pthread_mutex_init(&job.mu, NULL);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, kd_worker, &job);
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&job.mu);
+    free(tree.idx);
+    free(tree.axis);
+    return res;
+}

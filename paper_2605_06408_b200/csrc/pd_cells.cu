@@ -377,7 +377,8 @@ __device__ __forceinline__ uint32_t* coop_queue_mask() { return reinterpret_cast
 template <class T>
 constexpr size_t coop_smem_bytes() { return ((sizeof(CoopJob) + 15) & ~(size_t)15) + 2 * sizeof(float4) * T::QMAX + 4 * T::QC; }
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+    // barrier.sync (not the .aligned bar.sync): legal where the compiler has not reconverged the warp
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // Exact polytope-vs-box node test (not in the paper; strictly tighter than any AABB bound).  The
@@ -450,24 +451,30 @@ struct Box6 {
 
 // Warp-reduce the partial boxes into the cell AABB (widened by 2 ulp) and its radius bounds.
 __device__ __forceinline__ void finish_aabb(Cell& c, const Box6& b) {
-    float lo0 = b.lo0, lo1 = b.lo1, lo2 = b.lo2, hi0 = b.hi0, hi1 = b.hi1, hi2 = b.hi2;
-    c.flo[0] = iford(__reduce_min_sync(FULL, ford(lo0)));
-    c.flo[1] = iford(__reduce_min_sync(FULL, ford(lo1)));
-    c.flo[2] = iford(__reduce_min_sync(FULL, ford(lo2)));
-    c.fhi[0] = iford(__reduce_max_sync(FULL, ford(hi0)));
-    c.fhi[1] = iford(__reduce_max_sync(FULL, ford(hi1)));
-    c.fhi[2] = iford(__reduce_max_sync(FULL, ford(hi2)));
+    float lo[3], hi[3];
+    lo[0] = iford(__reduce_min_sync(FULL, ford(b.lo0)));
+    lo[1] = iford(__reduce_min_sync(FULL, ford(b.lo1)));
+    lo[2] = iford(__reduce_min_sync(FULL, ford(b.lo2)));
+    hi[0] = iford(__reduce_max_sync(FULL, ford(b.hi0)));
+    hi[1] = iford(__reduce_max_sync(FULL, ford(b.hi1)));
+    hi[2] = iford(__reduce_max_sync(FULL, ford(b.hi2)));
     float rm2 = 0.f, vm = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         // the FP32 copies are rounded to nearest: widen by 2 ulp so the box contains the FP64 cell
-        c.flo[k] -= fabsf(c.flo[k]) * 2.4e-7f + 1e-30f;
-        c.fhi[k] += fabsf(c.fhi[k]) * 2.4e-7f + 1e-30f;
-        rm2 += fmaxf(c.flo[k] * c.flo[k], c.fhi[k] * c.fhi[k]);
-        vm = fmaxf(vm, fmaxf(-c.flo[k], c.fhi[k]));
+        lo[k] -= fabsf(lo[k]) * 2.4e-7f + 1e-30f;
+        hi[k] += fabsf(hi[k]) * 2.4e-7f + 1e-30f;
+        rm2 += fmaxf(lo[k] * lo[k], hi[k] * hi[k]);
+        vm = fmaxf(vm, fmaxf(-lo[k], hi[k]));
     }
+    // every lane writes the same warp-uniform fields: no lane may still be reading the old ones, and all
+    // writes land before any lane reads the new ones
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { c.flo[k] = lo[k]; c.fhi[k] = hi[k]; }
     c.rmax = sqrtf(rm2);
     c.vmax = vm;
+    __syncwarp();
 }
 
 // Cell AABB (and, in SPHERE tiers, a bounding sphere centred at the previous AABB's centre: any
@@ -505,6 +512,7 @@ __device__ PD_INL_AABB void update_aabb(const WarpState<T>& S, Cell& c, int lane
         // FP32 vertex copies are within 2^-24 |v| of the FP64 cell: 1e-6 vmax covers it
         c.sc[0] = m0; c.sc[1] = m1; c.sc[2] = m2;
         c.srad = sqrtf(r2) * (1.f + 1e-6f) + 1e-6f * c.vmax;
+        __syncwarp();
     }
 }
 
@@ -1741,6 +1749,7 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(con
             c.px = site.x; c.py = site.y; c.pz = site.z; c.pw = site.w;
             c.self = s;
             c.self_orig = __ldg(&P.perm[s]);
+            __syncwarp();  // warp-uniform cell fields written by every lane
 #if PD_PROFILE
             const long long t_cell = clock64();
 #endif
