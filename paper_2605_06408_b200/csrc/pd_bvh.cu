@@ -333,6 +333,7 @@ cudaError_t bvh_gather(const float4* sites, const uint32_t* perm, int64_t n, flo
 
 cudaError_t bvh_topology(const uint64_t* keys_sorted, const float4* sorted, int n, int leaf, BvhScratch& sc, Bvh& out,
                          cudaStream_t st, int* launches) {
+    cudaMemsetAsync(sc.counters, 0, sizeof(int) * kCollapseCounters, st);  // [1] is read back after the cells
     if (n <= 1) {
         k_root_single<<<1, 1, 0, st>>>(out.root);
         ++*launches;
@@ -341,7 +342,6 @@ cudaError_t bvh_topology(const uint64_t* keys_sorted, const float4* sorted, int 
     k_karras<<<blocks(n - 1, 256), 256, 0, st>>>(keys_sorted, n, sc.child, sc.range, sc.parent_int, sc.parent_leaf);
     cudaMemsetAsync(sc.visit, 0, sizeof(int) * (size_t)(n - 1), st);
     k_refit<<<blocks(n, 256), 256, 0, st>>>(sorted, n, sc.child, sc.parent_int, sc.parent_leaf, sc.visit, sc.blo, sc.bhi);
-    cudaMemsetAsync(sc.counters, 0, sizeof(int) * kCollapseCounters, st);
     k_root<<<1, 1, 0, st>>>(sc.blo, sc.bhi, n, leaf, out.root, sc.tasks[0], sc.counters);
     *launches += 3;
     out.n_wide = 0;

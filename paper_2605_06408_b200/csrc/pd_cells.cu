@@ -165,9 +165,14 @@ struct __align__(16) WarpState {
         };
         struct {                  // finalize (the queue is dead by then)
             uint16_t tw[3][T::VMAX];  // twin vertex across edges a->b, b->c, c->a
-            int32_t nb_id[T::PMAX];   // neighbour staging
-            float nb_area[T::PMAX];
-            double farea[T::PMAX];    // face areas
+            union {
+                uint32_t etab[256];   // edge hash (tier 1): unordered plane pair -> its two vertices
+                struct {
+                    int32_t nb_id[T::PMAX];   // neighbour staging
+                    float nb_area[T::PMAX];
+                    double farea[T::PMAX];    // face areas
+                };
+            };
         };
     };
     uint16_t rem[T::VMAX];        // removed-vertex slots of the current clip
@@ -1383,6 +1388,115 @@ __device__ __forceinline__ void areas_range(WarpState<T>& S, int nv, int np, int
     }
 }
 
+// Tier 1 (<= 64 planes, <= 127 vertices): twins from a 256-entry edge hash and face areas by walking each
+// face's loop (lane = face), O(V) per cell instead of the O(V^2) scans above.  Every edge {x, y} of the closed
+// polytope is held by exactly two vertices (as x->y and y->x): entry = key(12) | A(7) | B(7), 127 = none.
+// A third holder or a missing partner is a topology failure (PD_CELL_DEGRADED).
+template <class T>
+constexpr bool kHashTwins = T::PMAX <= 64 && T::VMAX <= 127 && !T::COOP;
+constexpr uint32_t kEtEmpty = 0xffffffffu;
+__device__ __forceinline__ int et_hash(uint32_t key) { return (int)((key * 2654435761u) >> 24); }
+
+template <class T>
+__device__ __forceinline__ bool twins_hash(WarpState<T>& S, int nv, int lane) {
+    bool bad = false;
+    for (int k = lane; k < 256; k += 32) S.etab[k] = kEtEmpty;
+    __syncwarp();
+    for (int u = lane; u < nv; u += 32) {
+        const auto t = S.vt[u];
+        const int p[3] = {ta(t), tb(t), tc(t)};
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            const int x = p[e], y = p[e == 2 ? 0 : e + 1];
+            const uint32_t key = (uint32_t)(min(x, y) << 6 | max(x, y));
+            int h = et_hash(key);
+            for (int probe = 0; probe < 256; ++probe) {
+                const uint32_t w = S.etab[h];
+                if (w == kEtEmpty) {
+                    if (atomicCAS(&S.etab[h], kEtEmpty, key << 14 | (uint32_t)u << 7 | 127u) == kEtEmpty) break;
+                    --probe;  // lost the race for this slot: look at it again
+                    continue;
+                }
+                if ((w >> 14) == key) {
+                    if ((w & 127u) != 127u) { bad = true; break; }  // a third vertex on one edge
+                    if (atomicCAS(&S.etab[h], w, (w & ~127u) | (uint32_t)u) == w) break;
+                    --probe;
+                    continue;
+                }
+                h = (h + 1) & 255;
+            }
+        }
+    }
+    __syncwarp();
+    for (int u = lane; u < nv; u += 32) {
+        const auto t = S.vt[u];
+        const int p[3] = {ta(t), tb(t), tc(t)};
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+            const int x = p[e], y = p[e == 2 ? 0 : e + 1];
+            const uint32_t key = (uint32_t)(min(x, y) << 6 | max(x, y));
+            int h = et_hash(key);
+            uint32_t w = S.etab[h];
+            while (w != kEtEmpty && (w >> 14) != key) { h = (h + 1) & 255; w = S.etab[h]; }
+            int tw = 0xffff;
+            if (w != kEtEmpty) {
+                const int a = (int)(w >> 7) & 127, b = (int)(w & 127u);
+                tw = a == u ? b : a;
+                if (tw == 127) tw = 0xffff;
+            }
+            bad |= tw == 0xffff;
+            S.tw[e][u] = (uint16_t)tw;  // e = 0: across a->b, 1: b->c, 2: c->a (as twins_range)
+        }
+    }
+    __syncwarp();
+    return bad;
+}
+
+// Face areas by walking each face's vertex loop from its lowest vertex slot (deterministic order), lane = face.
+template <class T>
+__device__ __forceinline__ bool areas_walk(WarpState<T>& S, int nv, int np, int lane, double& vol, double& surf) {
+    uint32_t* start = S.bnd;  // dead outside clip(): the lowest vertex slot of every face
+    for (int f = lane; f < np; f += 32) start[f] = 0xffffffffu;
+    __syncwarp();
+    for (int u = lane; u < nv; u += 32) {
+        const auto t = S.vt[u];
+        atomicMin(&start[ta(t)], (uint32_t)u);
+        atomicMin(&start[tb(t)], (uint32_t)u);
+        atomicMin(&start[tc(t)], (uint32_t)u);
+    }
+    __syncwarp();
+    bool bad = false;
+    for (int f = lane; f < np; f += 32) {
+        double Ax = 0, Ay = 0, Az = 0;
+        const uint32_t s0 = start[f];
+        if (s0 != 0xffffffffu) {
+            int u = (int)s0;
+            double ux = S.vx[u], uy = S.vy[u], uz = S.vz[u];
+            for (int step = 0; step < T::VMAX; ++step) {
+                const auto t = S.vt[u];
+                const int slot = ta(t) == f ? 2 : (tb(t) == f ? 0 : (tc(t) == f ? 1 : -1));
+                const int w = slot < 0 ? 0xffff : S.tw[slot][u];
+                if (w == 0xffff) { bad = true; break; }
+                const double wx = S.vx[w], wy = S.vy[w], wz = S.vz[w];
+                Ax += uy * wz - uz * wy;
+                Ay += uz * wx - ux * wz;
+                Az += ux * wy - uy * wx;
+                u = w; ux = wx; uy = wy; uz = wz;
+                if (u == (int)s0) break;
+                if (step == T::VMAX - 1) bad = true;  // the loop never closed
+            }
+        }
+        Ax *= 0.5; Ay *= 0.5; Az *= 0.5;
+        const double area = sqrt(Ax * Ax + Ay * Ay + Az * Az);
+        S.farea[f] = area;
+        const double4 pl = S.pl[f];
+        const double nn = pl.x * pl.x + pl.y * pl.y + pl.z * pl.z;
+        vol += (Ax * pl.x + Ay * pl.y + Az * pl.z) * pl.w / nn;
+        surf += area;
+    }
+    return bad;
+}
+
 // One warp's share of a cooperative job (warp w of T::WARPS; warp 0 is the cell's own warp).
 template <class T>
 __device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int lane) {
@@ -1612,6 +1726,12 @@ __device__ __noinline__ unsigned finalize(WarpState<T>& S, Cell& c, int lane, co
         for (int w = 0; w < T::WARPS; ++w) { vol += J.dpart[w][0]; surf += J.dpart[w][1]; missing |= J.ipart[w][0] != 0; }
         vol /= 3.0;
         if (missing && lane == 0) c.degraded = 1;
+    } else if (kHashTwins<T>) {
+        bool bad = twins_hash(S, c.nv, lane);
+        bad |= areas_walk(S, c.nv, c.np, lane, vol, surf);
+        vol = warp_sum_d(vol) / 3.0;
+        surf = warp_sum_d(surf);
+        if (__any_sync(FULL, bad) && lane == 0) c.degraded = 1;
     } else {
         twins_range(S, c.nv, lane, 32);
         __syncwarp();
