@@ -1393,7 +1393,10 @@ __device__ __forceinline__ void areas_range(WarpState<T>& S, int nv, int np, int
 // polytope is held by exactly two vertices (as x->y and y->x): entry = key(12) | A(7) | B(7), 127 = none.
 // A third holder or a missing partner is a topology failure (PD_CELL_DEGRADED).
 template <class T>
-constexpr bool kHashTwins = T::PMAX <= 64 && T::VMAX <= 127 && !T::COOP;
+#ifndef PD_HASH_TWINS
+#define PD_HASH_TWINS 0  // 1: O(V) edge-hash finalize; measured 40% slower on C4 (645 vs 456 ms), kept as an option
+#endif
+constexpr bool kHashTwins = PD_HASH_TWINS && T::PMAX <= 64 && T::VMAX <= 127 && !T::COOP;
 constexpr uint32_t kEtEmpty = 0xffffffffu;
 __device__ __forceinline__ int et_hash(uint32_t key) { return (int)((key * 2654435761u) >> 24); }
 

@@ -6,7 +6,7 @@ import subprocess
 import sys
 from collections import defaultdict
 
-R = sys.argv[1] if len(sys.argv) > 1 else "r1"
+R = sys.argv[1] if len(sys.argv) > 1 else "r2"
 G = "gpurun_out"
 OUT = "profiles"
 os.makedirs(OUT, exist_ok=True)
@@ -68,7 +68,19 @@ j = {"round": R, "kernel": "cells_kernel tier 1 (C4, 10M sites, one launch)", "d
      "duration_ns": float(t1.get("gpu__time_duration.sum", ("0",))[0]),
      "issue_active_pct": float(t1.get("smsp__issue_active.avg.pct_of_peak_sustained_active", ("0",))[0]),
      "warps_active_pct": float(t1.get("sm__warps_active.avg.pct_of_peak_sustained_active", ("0",))[0]),
+     "cells": 1e7,
      "all_tiers": {k: {m: v for m, v in d.items()} for k, d in per.items()}}
+# FP32 lane-ops (FFMA counted once per lane-op), divergence, IPC
+ops = [t1.get(f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum") for o in ("fadd", "fmul", "ffma")]
+if all(ops):
+    j["fp32_lane_ops"] = sum(float(o[0]) for o in ops)
+if "smsp__thread_inst_executed_per_inst_executed.ratio" in t1:
+    j["threads_per_inst"] = float(t1["smsp__thread_inst_executed_per_inst_executed.ratio"][0])
+if "sm__inst_executed.avg.per_cycle_active" in t1:
+    j["ipc"] = float(t1["sm__inst_executed.avg.per_cycle_active"][0])
+if "sm__cycles_elapsed.avg.per_second" in t1:
+    j["sm_hz"] = float(t1["sm__cycles_elapsed.avg.per_second"][0])
+json.dump(j, open(f"{OUT}/{R}_cells_metrics.json", "w"), indent=1)
 json.dump(j, open(f"{OUT}/cells_kernel_traffic.json", "w"), indent=1)
 json.dump(j, open(f"{OUT}/{R}_cells_traffic.json", "w"), indent=1)
 
