@@ -54,6 +54,12 @@ def lib():
         L.orc_copy.argtypes = [P, P, P, P, P, P, P]
         L.orc_run_kdtree.restype = P
         L.orc_run_kdtree.argtypes = [P, P, ctypes.c_int64, P, P, ctypes.c_int64, ctypes.c_int]
+        L.orc_kd_build.restype = P
+        L.orc_kd_build.argtypes = [P, P, ctypes.c_int64, P]
+        L.orc_kd_run.restype = P
+        L.orc_kd_run.argtypes = [P, P, ctypes.c_int64, ctypes.c_int]
+        L.orc_kd_free.restype = None
+        L.orc_kd_free.argtypes = [P]
         L.orc_counts.restype = None
         L.orc_counts.argtypes = [P, P, P]
         L.orc_free.restype = None
@@ -93,21 +99,7 @@ def _prep(points, weights, box):
     return pts, w, bx
 
 
-def cells(points, weights, box, ids=None, threads: int | None = None, order_k: int = 64,
-          kdtree: bool = False) -> OracleCells:
-    """Oracle cells for `ids` (default: all).  box = (lo.x, lo.y, lo.z, hi.x, hi.y, hi.z).
-    kdtree=True: the CPU reference of the same definition instead (pd_oracle.c orc_run_kdtree: the same
-    clipper, candidates in ascending distance from a k-d tree, stopped by the radius of security) -- a
-    reported CPU baseline (SURVEY.md §8(d)(ii)); the parity tests use the brute-force oracle."""
-    pts, w, bx = _prep(points, weights, box)
-    n = pts.shape[0]
-    ids = np.arange(n, dtype=np.int64) if ids is None else np.ascontiguousarray(np.asarray(ids, dtype=np.int64))
-    threads = threads or os.cpu_count() or 1
-    L = lib()
-    if kdtree:
-        r = L.orc_run_kdtree(_ptr(pts), _ptr(w), n, _ptr(bx), _ptr(ids), len(ids), int(threads))
-    else:
-        r = L.orc_run(_ptr(pts), _ptr(w), n, _ptr(bx), _ptr(ids), len(ids), int(threads), int(order_k))
+def _collect(L, r, ids) -> OracleCells:
     try:
         nnz = L.orc_nnz(r)
         m = len(ids)
@@ -124,6 +116,53 @@ def cells(points, weights, box, ids=None, threads: int | None = None, order_k: i
     finally:
         L.orc_free(r)
     return OracleCells(ids, off, nbr[:nnz], area[:nnz], vol, surf, flags, dropped, small)
+
+
+class KdReference:
+    """The CPU reference of the same definition (pd_oracle.c orc_kd_*): a k-d tree with
+    per-subtree bounding box and max weight, built once per point set; `cells(ids)` walks it best-first per
+    cell and stops at the weighted radius of security.  A reported CPU baseline, not the parity oracle."""
+
+    def __init__(self, points, weights, box):
+        self.pts, self.w, self.bx = _prep(points, weights, box)
+        self.n = self.pts.shape[0]
+        self._L = lib()
+        self._h = self._L.orc_kd_build(_ptr(self.pts), _ptr(self.w), self.n, _ptr(self.bx))
+
+    def cells(self, ids=None, threads: int | None = None) -> OracleCells:
+        ids = np.arange(self.n, dtype=np.int64) if ids is None else np.ascontiguousarray(np.asarray(ids, np.int64))
+        r = self._L.orc_kd_run(self._h, _ptr(ids), len(ids), int(threads or os.cpu_count() or 1))
+        return _collect(self._L, r, ids)
+
+    def close(self):
+        if self._h:
+            self._L.orc_kd_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def cells(points, weights, box, ids=None, threads: int | None = None, order_k: int = 64,
+          kdtree: bool = False) -> OracleCells:
+    """Oracle cells for `ids` (default: all).  box = (lo.x, lo.y, lo.z, hi.x, hi.y, hi.z).
+    kdtree=True: the CPU reference of the same definition instead (pd_oracle.c orc_run_kdtree: the same
+    clipper, fed by a best-first walk of a weight-augmented k-d tree, stopped by the weighted radius of
+    security) -- a
+    reported CPU baseline (SURVEY.md §8(d)(ii)); the parity tests use the brute-force oracle."""
+    pts, w, bx = _prep(points, weights, box)
+    n = pts.shape[0]
+    ids = np.arange(n, dtype=np.int64) if ids is None else np.ascontiguousarray(np.asarray(ids, dtype=np.int64))
+    threads = threads or os.cpu_count() or 1
+    L = lib()
+    if kdtree:
+        r = L.orc_run_kdtree(_ptr(pts), _ptr(w), n, _ptr(bx), _ptr(ids), len(ids), int(threads))
+    else:
+        r = L.orc_run(_ptr(pts), _ptr(w), n, _ptr(bx), _ptr(ids), len(ids), int(threads), int(order_k))
+    return _collect(L, r, ids)
 
 
 @dataclass

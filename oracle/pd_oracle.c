@@ -522,96 +522,105 @@ int orc_cell_geometry(const float* pts, const float* w, int64_t n, const double*
 
 /* ==============================================================================================
  * CPU reference of the same definition (a reported baseline, NOT the oracle the
- * parity tests use): the oracle's clipper above, fed candidates in ascending distance from a k-d tree and
- * stopped by the radius of security (the exact early reject of build_cell turned into a termination test,
- * the prior-work idea PAPER.md:126, :221): with c = w_i - w_max, the plane of every site at distance
- * >= D lies at distance >= (D^2 + c)/(2D) from p_i, which is increasing in D once D^2 >= max(0, c); so once
- * that bound reaches R_max(1+1e-12), no further candidate can cut (same implication as build_cell's skip).
- * The polytope is the same set as the oracle's (exact arithmetic: clip order is irrelevant); rounding
- * differs, so tests compare it with the comparator's tolerances.  Multithreaded over cells.
+ * parity tests use).  The oracle's clipper above, fed by a best-first walk of a k-d tree whose every
+ * subtree carries its bounding box and the largest weight in it (the CPU analogue of the paper's
+ * weight-augmented BVH), and stopped by the radius of security (prior work,
+ * PAPER.md:126, :221) in its weighted form:
+ *   a site j at distance D >= d from p_i with w_j <= w_max has its plane at distance
+ *   d_ij = (D^2 + w_i - w_j)/(2D) >= f(D) = (D^2 + c)/(2D), c = w_i - w_max
+ *   and min_{D >= d} f(D) = f(d) if c <= 0 or d^2 >= c, else sqrt(c)  (f decreases up to sqrt(c)).
+ * Subtrees are visited in ascending order of that lower bound; once it reaches R_max (1 + 1e-12), no
+ * remaining site can cut the cell -- the same implication as build_cell's exact skip.  Exact arithmetic
+ * gives the oracle's polytope (clip order is irrelevant); rounding differs, so the tests compare the two
+ * with the comparator's tolerances.  Multithreaded over cells; the tree is built once per point set.
  * ============================================================================================== */
 
 typedef struct {
-    const orc_input* in;
-    int32_t* idx;      /* permutation of 0..n-1, kd-ordered */
-    int32_t* axis;     /* per implicit node (mid index): split axis */
-    double wmax;
-} kd_tree;
+    orc_input in;
+    int32_t* idx;      /* permutation of 0..n-1, kd-ordered; subtree [b,e) is keyed by its mid (b+e)/2 */
+    int32_t* axis;     /* per key: split axis */
+    double* bb;        /* per key: bounding box of the subtree's sites (lo.xyz, hi.xyz) */
+    double* wmax;      /* per key: largest weight in the subtree */
+} orc_kd;
 
 static double coord(const orc_input* in, int32_t j, int ax) { return (double)in->pts[3 * (int64_t)j + ax]; }
 
-static void kd_build_rec(kd_tree* t, int64_t b, int64_t e) {
-    if (e - b <= 1) return;
+static void kd_build_rec(orc_kd* t, int64_t b, int64_t e) {
+    if (e <= b) return;
+    int64_t mid = (b + e) / 2;
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-    for (int64_t k = b; k < e; ++k)
+    double wm = -1e300;
+    for (int64_t k = b; k < e; ++k) {
         for (int a = 0; a < 3; ++a) {
-            double v = coord(t->in, t->idx[k], a);
+            double v = coord(&t->in, t->idx[k], a);
             if (v < lo[a]) lo[a] = v;
             if (v > hi[a]) hi[a] = v;
         }
+        double wk = wt(&t->in, t->idx[k]);
+        if (wk > wm) wm = wk;
+    }
     int ax = 0;
     for (int a = 1; a < 3; ++a) if (hi[a] - lo[a] > hi[ax] - lo[ax]) ax = a;
-    int64_t mid = (b + e) / 2;
     /* quickselect the median on axis ax (ties broken by index: deterministic) */
     int64_t l = b, r = e - 1;
     while (l < r) {
         int32_t piv = t->idx[(l + r) / 2];
-        double pv = coord(t->in, piv, ax);
+        double pv = coord(&t->in, piv, ax);
         int64_t i = l, j = r;
         while (i <= j) {
-            while (coord(t->in, t->idx[i], ax) < pv || (coord(t->in, t->idx[i], ax) == pv && t->idx[i] < piv)) ++i;
-            while (coord(t->in, t->idx[j], ax) > pv || (coord(t->in, t->idx[j], ax) == pv && t->idx[j] > piv)) --j;
+            while (coord(&t->in, t->idx[i], ax) < pv || (coord(&t->in, t->idx[i], ax) == pv && t->idx[i] < piv)) ++i;
+            while (coord(&t->in, t->idx[j], ax) > pv || (coord(&t->in, t->idx[j], ax) == pv && t->idx[j] > piv)) --j;
             if (i <= j) { int32_t s = t->idx[i]; t->idx[i] = t->idx[j]; t->idx[j] = s; ++i; --j; }
         }
         if (mid <= j) r = j; else if (mid >= i) l = i; else break;
     }
     t->axis[mid] = ax;
+    for (int a = 0; a < 3; ++a) { t->bb[6 * mid + a] = lo[a]; t->bb[6 * mid + 3 + a] = hi[a]; }
+    t->wmax[mid] = wm;
     kd_build_rec(t, b, mid);
     kd_build_rec(t, mid + 1, e);
 }
 
-typedef struct { kn_t* h; int n, k; } knn_heap;   /* max-heap on (key, j) of the k best */
-
-static int kn_less(const kn_t* a, const kn_t* b) { return a->key < b->key || (a->key == b->key && a->j < b->j); }
-static void kh_push(knn_heap* H, double key, int64_t j) {
-    kn_t x = {key, j};
-    if (H->n < H->k) {
-        int i = H->n++;
-        while (i > 0) { int p = (i - 1) / 2; if (!kn_less(&H->h[p], &x)) break; H->h[i] = H->h[p]; i = p; }
-        H->h[i] = x;
-    } else if (kn_less(&x, &H->h[0])) {
-        int i = 0;
-        for (;;) {
-            int l = 2 * i + 1, r = l + 1, m = -1;
-            kn_t* best = &x;
-            if (l < H->n && kn_less(best, &H->h[l])) { best = &H->h[l]; m = l; }
-            if (r < H->n && kn_less(best, &H->h[r])) { best = &H->h[r]; m = r; }
-            if (m < 0) break;
-            H->h[i] = H->h[m]; i = m;
-        }
-        H->h[i] = x;
+/* Lower bound of the plane distance d_ij over the subtree keyed `key` (see the header above). */
+static double kd_lower_bound(const orc_kd* t, int64_t key, v3 pi, double wi) {
+    const double* bb = t->bb + 6 * key;
+    double q[3] = {pi.x, pi.y, pi.z}, d2 = 0;
+    for (int a = 0; a < 3; ++a) {
+        double g = q[a] < bb[a] ? bb[a] - q[a] : (q[a] > bb[3 + a] ? q[a] - bb[3 + a] : 0.0);
+        d2 += g * g;
     }
+    double c = wi - t->wmax[key];
+    if (c > 0 && d2 < c) return sqrt(c);
+    if (d2 == 0) return -HUGE_VAL;
+    return (d2 + c) / (2.0 * sqrt(d2));
 }
 
-static void kd_knn_rec(const kd_tree* t, int64_t b, int64_t e, v3 q, knn_heap* H) {
-    if (e <= b) return;
-    int64_t mid = (b + e) / 2;
-    int32_t j = t->idx[mid];
-    v3 pj = site(t->in, j);
-    v3 d = v3sub(pj, q);
-    kh_push(H, v3dot(d, d), j);
-    if (e - b == 1) return;
-    int ax = t->axis[mid];
-    double diff = (ax == 0 ? q.x : ax == 1 ? q.y : q.z) - coord(t->in, j, ax);
-    int64_t nb = diff < 0 ? b : mid + 1, ne = diff < 0 ? mid : e;
-    int64_t fb = diff < 0 ? mid + 1 : b, fe = diff < 0 ? e : mid;
-    kd_knn_rec(t, nb, ne, q, H);
-    if (H->n < H->k || diff * diff <= H->h[0].key) kd_knn_rec(t, fb, fe, q, H);
+typedef struct { double lb; int64_t b, e; } kd_ent;
+typedef struct { kd_ent* h; int64_t n, cap; } kd_heap;   /* min-heap on lb */
+
+static void kdh_push(kd_heap* H, kd_ent x) {
+    if (H->n == H->cap) { H->cap = H->cap ? 2 * H->cap : 256; H->h = (kd_ent*)realloc(H->h, sizeof(kd_ent) * H->cap); }
+    int64_t i = H->n++;
+    while (i > 0) { int64_t p = (i - 1) / 2; if (H->h[p].lb <= x.lb) break; H->h[i] = H->h[p]; i = p; }
+    H->h[i] = x;
+}
+static kd_ent kdh_pop(kd_heap* H) {
+    kd_ent top = H->h[0], x = H->h[--H->n];
+    int64_t i = 0;
+    for (;;) {
+        int64_t l = 2 * i + 1, r = l + 1, m = i;
+        double best = x.lb;
+        if (l < H->n && H->h[l].lb < best) { m = l; best = H->h[l].lb; }
+        if (r < H->n && H->h[r].lb < best) { m = r; }
+        if (m == i) break;
+        H->h[i] = H->h[m]; i = m;
+    }
+    if (H->n > 0) H->h[i] = x;
+    return top;
 }
 
 typedef struct {
-    const orc_input* in;
-    const kd_tree* tree;
+    const orc_kd* tree;
     const int64_t* ids;
     int64_t ncells;
     orc_cell* out;
@@ -619,50 +628,41 @@ typedef struct {
     pthread_mutex_t mu;
 } kd_job;
 
-static int build_cell_kd(const orc_input* in, const kd_tree* tree, int64_t i, orc_ws* ws, kn_t** buf, int* bufcap,
-                         int* flags) {
+static int build_cell_kd(const orc_kd* tree, int64_t i, orc_ws* ws, kd_heap* H, int* flags) {
+    const orc_input* in = &tree->in;
     v3 pi = site(in, i);
     double wi = wt(in, i);
     int cur = 0, degraded = 0;
     *flags = 0;
     poly_init_box(&ws->P[cur], in->box, pi);
-    double rmax2 = poly_rmax2(&ws->P[cur]);
-    const double c = wi - tree->wmax;
-    int64_t k = 64, pos = 0;
-    for (;;) {
-        int64_t kq = k + 1 < in->n ? k + 1 : in->n;
-        if (*bufcap < kq) { *bufcap = (int)kq; *buf = (kn_t*)realloc(*buf, sizeof(kn_t) * kq); }
-        knn_heap H = {*buf, 0, (int)kq};
-        kd_knn_rec(tree, 0, in->n, pi, &H);
-        qsort(H.h, H.n, sizeof(kn_t), kn_cmp);
-        int stop = 0;
-        for (int64_t t = pos; t < H.n && !stop; ++t) {
-            int64_t j = H.h[t].j;
-            if (j == i) continue;
-            v3 D = v3sub(site(in, j), pi);
-            double D2 = v3dot(D, D);
-            double wj = wt(in, j);
-            if (D2 == 0.0) {
-                if (wj > wi || (wj == wi && j < i)) { *flags |= ORC_EMPTY | ORC_DUPLICATE; return -1; }
-                continue;
-            }
-            double nD = sqrt(D2), rmax = sqrt(rmax2);
-            /* radius of security: every later candidate (distance >= nD) is beyond the cell */
-            if ((c <= 0 || D2 >= c) && (D2 + c) / (2 * nD) >= rmax * (1.0 + 1e-12)) { stop = 1; break; }
-            double dd = 0.5 * (D2 + wi - wj);
-            double dij = dd / nD;
-            if (dij >= rmax * (1.0 + 1e-12)) continue;   /* the oracle's exact skip */
-            double tau = 1e-13 * nD * rmax;
-            int r = poly_clip(&ws->P[cur], &ws->P[cur ^ 1], D, dd, (int)j, tau,
-                              &ws->segs, &ws->segcap, &ws->scratch, &ws->scap, &degraded);
-            if (r == 0) continue;
-            cur ^= 1;
-            if (r == 2) { *flags |= ORC_EMPTY; if (degraded) *flags |= ORC_DEGRADED; return -1; }
-            rmax2 = poly_rmax2(&ws->P[cur]);
+    double rmax = sqrt(poly_rmax2(&ws->P[cur]));
+    H->n = 0;
+    if (in->n > 0) { kd_ent root = {kd_lower_bound(tree, in->n / 2, pi, wi), 0, in->n}; kdh_push(H, root); }
+    while (H->n > 0) {
+        kd_ent x = kdh_pop(H);
+        if (x.lb >= rmax * (1.0 + 1e-12)) break;   /* radius of security: no remaining site can cut */
+        int64_t mid = (x.b + x.e) / 2;
+        if (mid > x.b) { kd_ent l = {kd_lower_bound(tree, (x.b + mid) / 2, pi, wi), x.b, mid}; kdh_push(H, l); }
+        if (x.e > mid + 1) { kd_ent r = {kd_lower_bound(tree, (mid + 1 + x.e) / 2, pi, wi), mid + 1, x.e}; kdh_push(H, r); }
+        int64_t j = tree->idx[mid];
+        if (j == i) continue;
+        v3 D = v3sub(site(in, j), pi);
+        double D2 = v3dot(D, D);
+        double wj = wt(in, j);
+        if (D2 == 0.0) {   /* coincident sites (Q5) */
+            if (wj > wi || (wj == wi && j < i)) { *flags |= ORC_EMPTY | ORC_DUPLICATE; return -1; }
+            continue;
         }
-        if (stop || H.n >= in->n) break;
-        pos = H.n;
-        k *= 4;
+        double nD = sqrt(D2);
+        double dd = 0.5 * (D2 + wi - wj);
+        if (dd / nD >= rmax * (1.0 + 1e-12)) continue;   /* the oracle's exact skip */
+        double tau = 1e-13 * nD * rmax;
+        int r = poly_clip(&ws->P[cur], &ws->P[cur ^ 1], D, dd, (int)j, tau,
+                          &ws->segs, &ws->segcap, &ws->scratch, &ws->scap, &degraded);
+        if (r == 0) continue;
+        cur ^= 1;
+        if (r == 2) { *flags |= ORC_EMPTY; if (degraded) *flags |= ORC_DEGRADED; return -1; }
+        rmax = sqrt(poly_rmax2(&ws->P[cur]));
     }
     if (degraded) *flags |= ORC_DEGRADED;
     return cur;
@@ -672,8 +672,7 @@ static void* kd_worker(void* arg) {
     kd_job* job = (kd_job*)arg;
     orc_ws ws;
     memset(&ws, 0, sizeof(ws));
-    kn_t* buf = NULL;
-    int bufcap = 0;
+    kd_heap H = {NULL, 0, 0};
     for (;;) {
         pthread_mutex_lock(&job->mu);
         int64_t t0 = job->next;
@@ -683,33 +682,42 @@ static void* kd_worker(void* arg) {
         int64_t t1 = t0 + 64 < job->ncells ? t0 + 64 : job->ncells;
         for (int64_t t = t0; t < t1; ++t) {
             int flags = 0;
-            int r = build_cell_kd(job->in, job->tree, job->ids[t], &ws, &buf, &bufcap, &flags);
+            int r = build_cell_kd(job->tree, job->ids[t], &ws, &H, &flags);
             finalize_cell(r >= 0 ? &ws.P[r] : NULL, &job->out[t], flags);
         }
     }
-    free(buf);
+    free(H.h);
     ws_free(&ws);
     return NULL;
 }
 
-/* Same outputs as orc_run (read with orc_nnz / orc_copy / orc_counts / orc_free). */
-orc_result* orc_run_kdtree(const float* pts, const float* w, int64_t n, const double* box, const int64_t* ids,
-                           int64_t ncells, int nthreads) {
-    orc_input in;
-    in.pts = pts; in.w = w; in.n = n; in.order_k = 0;
-    memcpy(in.box, box, sizeof(in.box));
-    kd_tree tree;
-    tree.in = &in;
-    tree.idx = (int32_t*)malloc(sizeof(int32_t) * (n > 0 ? n : 1));
-    tree.axis = (int32_t*)calloc(n > 0 ? n : 1, sizeof(int32_t));
-    tree.wmax = -1e300;
-    for (int64_t j = 0; j < n; ++j) { tree.idx[j] = (int32_t)j; if (wt(&in, j) > tree.wmax) tree.wmax = wt(&in, j); }
-    kd_build_rec(&tree, 0, n);
+/* Build the tree once per point set (the arrays are borrowed and must outlive the handle). */
+orc_kd* orc_kd_build(const float* pts, const float* w, int64_t n, const double* box) {
+    orc_kd* t = (orc_kd*)calloc(1, sizeof(orc_kd));
+    t->in.pts = pts; t->in.w = w; t->in.n = n; t->in.order_k = 0;
+    memcpy(t->in.box, box, sizeof(t->in.box));
+    int64_t m = n > 0 ? n : 1;
+    t->idx = (int32_t*)malloc(sizeof(int32_t) * m);
+    t->axis = (int32_t*)calloc(m, sizeof(int32_t));
+    t->bb = (double*)malloc(sizeof(double) * 6 * m);
+    t->wmax = (double*)malloc(sizeof(double) * m);
+    for (int64_t j = 0; j < n; ++j) t->idx[j] = (int32_t)j;
+    kd_build_rec(t, 0, n);
+    return t;
+}
+
+void orc_kd_free(orc_kd* t) {
+    if (!t) return;
+    free(t->idx); free(t->axis); free(t->bb); free(t->wmax); free(t);
+}
+
+/* Cells ids[0..ncells) from a built tree; same outputs as orc_run (orc_nnz / orc_copy / orc_counts / orc_free). */
+orc_result* orc_kd_run(const orc_kd* tree, const int64_t* ids, int64_t ncells, int nthreads) {
     orc_result* res = (orc_result*)calloc(1, sizeof(orc_result));
     res->ncells = ncells;
     res->cells = (orc_cell*)calloc(ncells > 0 ? ncells : 1, sizeof(orc_cell));
     kd_job job;
-    job.in = &in; job.tree = &tree; job.ids = ids; job.ncells = ncells; job.out = res->cells; job.next = 0;
+    job.tree = tree; job.ids = ids; job.ncells = ncells; job.out = res->cells; job.next = 0;
     pthread_mutex_init(&job.mu, NULL);
     if (nthreads < 1) nthreads = 1;
     if (nthreads > 256) nthreads = 256;
@@ -717,7 +725,13 @@ orc_result* orc_run_kdtree(const float* pts, const float* w, int64_t n, const do
     for (int t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, kd_worker, &job);
     for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
     pthread_mutex_destroy(&job.mu);
-    free(tree.idx);
-    free(tree.axis);
     return res;
+}
+
+orc_result* orc_run_kdtree(const float* pts, const float* w, int64_t n, const double* box, const int64_t* ids,
+                           int64_t ncells, int nthreads) {
+    orc_kd* t = orc_kd_build(pts, w, n, box);
+    orc_result* r = orc_kd_run(t, ids, ncells, nthreads);
+    orc_kd_free(t);
+    return r;
 }

@@ -357,3 +357,37 @@ def test_dual_tets_cube_corner_and_two_sites():
     t, _ = oracle.dual_tets(P, None, box)
     # the centre site 0 lies inside the tetrahedron of the other four: Delaunay = 4 tets around it
     assert sorted(map(tuple, t.tolist())) == [(0, 1, 2, 3), (0, 1, 2, 4), (0, 1, 3, 4), (0, 2, 3, 4)]
+
+
+# ----------------------------------------------------------------------------- CPU reference (bench baseline)
+
+class _Rows:
+    pass
+
+
+@pytest.mark.parametrize("cfg,n", [("C1", None), ("C2", 4000), ("C3", 4000), ("C4", 4000), ("C5", 4000)])
+def test_cpu_reference_same_definition(cfg, n):
+    """The k-d tree + weighted radius-of-security CPU reference reaches the oracle's cells:
+    it only skips sites whose bisector provably misses the cell."""
+    from compare import compare
+    wl = pdgen.make(cfg, n=n)
+    k = oracle.KdReference(wl.points, wl.weights, wl.box).cells()
+    o = oracle.cells(wl.points, wl.weights, wl.box)
+    d = _Rows()
+    d.offsets, d.neighbors, d.areas, d.surface, d.flags = k.offsets, k.nbr, k.area, k.surf, k.flags
+    d.volumes = k.vol.astype(np.float32)
+    rep = compare(d, o)
+    assert rep.ok, rep.summary()
+    assert rep.cells == wl.n
+
+
+def test_cpu_reference_duplicates_and_empty():
+    """Coincident sites (Q5) and weight-emptied cells: the walk must still meet the owner / the dominating site."""
+    pts = np.array([[0.5, 0.5, 0.5], [0.5, 0.5, 0.5], [0.2, 0.3, 0.4], [0.8, 0.7, 0.6], [0.25, 0.3, 0.4]], np.float32)
+    w = np.array([0.0, 0.01, 0.0, 0.0, 0.5], np.float32)
+    box = (0, 0, 0, 1, 1, 1)
+    k = oracle.KdReference(pts, w, box).cells()
+    o = oracle.cells(pts, w, box)
+    assert np.array_equal(k.flags, o.flags)
+    assert np.allclose(k.vol, o.vol, rtol=1e-9, atol=1e-15)
+    assert k.flags[0] & oracle.DUPLICATE and k.flags[2] & oracle.EMPTY
