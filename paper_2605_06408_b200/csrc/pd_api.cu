@@ -557,6 +557,12 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         int* tovf = want_tets ? W.alloc<int>(1) : nullptr;
         int4* tarena = nullptr;
         int64_t tcap = std::max<int64_t>((end - begin) * 8, 4096);
+        // deferred tier-1 finalize (pd_cells.cu finalize_kernel): per-cell topology records, ~60 words per
+        // cell on average (2 + planes + vertices); a cell that does not fit is finalized in the cell kernel
+        const bool defer = !getenv("PD_DEFER") || atoi(getenv("PD_DEFER")) != 0;
+        uint32_t* rec_index = defer ? W.alloc<uint32_t>((size_t)std::max<int64_t>(n, 1)) : nullptr;
+        const int64_t rec_cap = std::min<int64_t>(std::max<int64_t>((end - begin) * 80, 1 << 16), 0xfffffff0LL);
+        uint32_t* rec_arena = defer ? W.alloc<uint32_t>((size_t)rec_cap) : nullptr;
         for (int attempt = 0; attempt < 3; ++attempt) {
             anbr = W.alloc<int32_t>(cap);
             if (want_tets) {
@@ -584,6 +590,13 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.root = bvh.root;
             for (int k = 0; k < 3; ++k) { P.box_lo[k] = hbox[k]; P.box_hi[k] = hbox[3 + k]; }
             P.flags = opt.flags;
+            if (defer && end > begin) {
+                ck(cudaMemsetAsync(rec_index + begin, 0xff, sizeof(uint32_t) * (size_t)(end - begin), st));
+                P.rec_index = rec_index;
+                P.rec_arena = rec_arena;
+                P.rec_top = counters + 6;
+                P.rec_cap = rec_cap;
+            }
             if (opt.flags & PD_WARM_ADAPTIVE) P.flags = (P.flags & ~PD_WARM_ADAPTIVE) | PD_WARM_START;
             P.out.cnt = cnt;
             P.out.aoff = aoff;

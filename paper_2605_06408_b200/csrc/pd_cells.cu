@@ -164,12 +164,23 @@ struct __align__(16) WarpState {
             float qkey[PD_LAZY_POP ? T::QMAX : 1];  // priority at push time (lazy pop only)
         };
         struct {                  // finalize (the queue is dead by then)
-            uint16_t tw[3][T::VMAX];  // twin vertex across edges a->b, b->c, c->a
+            union {
+                uint16_t tw[3][T::VMAX];     // twin vertex across edges a->b, b->c, c->a
+                uint16_t flist[3 * T::VMAX]; // face walk (tier 1): vertices bucketed by face, u | y << 7
+            };
             union {
                 uint32_t etab[256];   // edge hash (tier 1): unordered plane pair -> its two vertices
                 struct {
-                    int32_t nb_id[T::PMAX];   // neighbour staging
-                    float nb_area[T::PMAX];
+                    union {
+                        struct {
+                            int32_t nb_id[T::PMAX];   // neighbour staging
+                            float nb_area[T::PMAX];
+                        };
+                        struct {                      // face walk: per-face CSR offsets and fill cursors
+                            uint32_t fcnt[T::PMAX];
+                            uint32_t ffill[T::PMAX];
+                        };
+                    };
                     double farea[T::PMAX];    // face areas
                 };
             };
@@ -292,8 +303,12 @@ struct Counters {
 // more).  m = 1e-6 (|n|_1 vmax + |D|^2 + |w_i - w_j|) is > 8x the worst-case error.
 struct FPlane {
     float nx, ny, nz, d, m;
-    float tl;  // FP64 certification tolerance 1e-12 |n| R (reading R9), precomputed in FP32
 };
+// FP64 certification tolerance 1e-12 |n| R (reading R9), in FP32; only evaluated on the rare certification path.
+__device__ __forceinline__ float cert_tol(const FPlane& f, float rmax) {
+    const float f2 = f.nx * f.nx + f.ny * f.ny + f.nz * f.nz;
+    return 1e-12f * (f2 * rsqrtf(f2)) * rmax;
+}
 
 // r^2 of the directional radius for an octant set (one corner per octant is
 // sound).  allow bit 2k: + side on axis k; bit 2k+1: - side.
@@ -620,7 +635,7 @@ __device__ __noinline__ int rem_from_omask(WarpState<T>& S, int nch, int lane) {
 // hot loop carries no FP64 set-up.
 __device__ __forceinline__ bool outside_fp64(const Cell& c, float4 sj, const FPlane& f, double vx, double vy, double vz) {
     const double4 pe = exact_plane(c, sj);
-    return fma(pe.x, vx, fma(pe.y, vy, pe.z * vz)) - pe.w > (double)f.tl;
+    return fma(pe.x, vx, fma(pe.y, vy, pe.z * vz)) - pe.w > (double)cert_tol(f, c.rmax);
 }
 
 template <class T>
@@ -992,10 +1007,6 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         }
         const int jsrc = __shfl_sync(FULL, j, src);
         const float4 sjs = __ldg(&P.sites[jsrc]);  // the site itself (FP64 plane of the certification)
-        {
-            const float f2 = f.nx * f.nx + f.ny * f.ny + f.nz * f.nz;
-            f.tl = 1e-12f * (f2 * rsqrtf(f2)) * c.rmax;
-        }
         PT_BEGIN(t_clip);
         int st = clip(S, c, lane, sjs, f, jsrc, cnt);
         PT_END(t_clip, 3);
@@ -1500,6 +1511,95 @@ __device__ __forceinline__ bool areas_walk(WarpState<T>& S, int nv, int np, int 
     return bad;
 }
 
+// Tier 1 (<= 64 planes, <= 128 vertices, one warp): face areas by walking each face's vertex loop, lane = face,
+// with the vertices bucketed by face first (CSR built with shared-memory atomics), O(sum_f k_f^2) per cell instead
+// of the O(V^2) twin scan + O(F V) area scan above.  Vertex u = (a, b, c) (CCW from outside) rotated to put face f
+// first, (f, y, z): its successor on face f's loop is the vertex whose rotated triplet is (f, z, .) -- the holder
+// of the reverse of u's dual edge z -> f, i.e. its twin (areas_range's tw[which][u]).  Each walk starts at the
+// lowest vertex slot of the face (deterministic summation order).  A face whose vertices do not form exactly one
+// cycle is a topology failure (PD_CELL_DEGRADED).
+#ifndef PD_FACE_WALK
+#define PD_FACE_WALK 1
+#endif
+template <class T>
+constexpr bool kFaceWalk = PD_FACE_WALK && T::PMAX <= 64 && T::VMAX <= 128 && !T::COOP && !T::GLOBAL;
+
+template <class T>
+__device__ __forceinline__ bool areas_facewalk(WarpState<T>& S, int nv, int np, int lane, double& vol, double& surf) {
+    uint32_t* const off = S.fcnt;
+    uint32_t* const cur = S.ffill;
+    uint16_t* const list = S.flist;
+    for (int f = lane; f < np; f += 32) { off[f] = 0u; cur[f] = 0u; }
+    __syncwarp();
+    for (int u = lane; u < nv; u += 32) {
+        const auto t = S.vt[u];
+        atomicAdd(&off[ta(t)], 1u);
+        atomicAdd(&off[tb(t)], 1u);
+        atomicAdd(&off[tc(t)], 1u);
+    }
+    __syncwarp();
+    {   // exclusive scan of the per-face counts (np <= 64: two faces per lane)
+        const int f0 = 2 * lane;
+        const uint32_t c0 = f0 < np ? off[f0] : 0u, c1 = f0 + 1 < np ? off[f0 + 1] : 0u;
+        uint32_t inc = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += v;
+        }
+        __syncwarp();
+        if (f0 < np) off[f0] = inc - c0 - c1;
+        if (f0 + 1 < np) off[f0 + 1] = inc - c1;
+    }
+    __syncwarp();
+    for (int u = lane; u < nv; u += 32) {
+        const auto t = S.vt[u];
+        const int a = ta(t), b = tb(t), cc = tc(t);
+        list[off[a] + atomicAdd(&cur[a], 1u)] = (uint16_t)(u | b << 7);   // on face a: (a, b, c), y = b
+        list[off[b] + atomicAdd(&cur[b], 1u)] = (uint16_t)(u | cc << 7);  // on face b: (b, c, a), y = c
+        list[off[cc] + atomicAdd(&cur[cc], 1u)] = (uint16_t)(u | a << 7); // on face c: (c, a, b), y = a
+    }
+    __syncwarp();
+    bool bad = false;
+    for (int f = lane; f < np; f += 32) {
+        const int o = (int)off[f], k = (int)cur[f];
+        double Ax = 0, Ay = 0, Az = 0;
+        if (k > 0) {
+            int u0 = 0x7fff;
+            for (int q = 0; q < k; ++q) u0 = min(u0, (int)(list[o + q] & 127u));
+            int u = u0, steps = 0;
+            double ux = S.vx[u], uy = S.vy[u], uz = S.vz[u];
+            for (;;) {
+                const auto t = S.vt[u];
+                const int a = ta(t), b = tb(t), cc = tc(t);
+                const int z = a == f ? cc : (b == f ? a : b);  // u's plane before f (CCW)
+                int w = -1;
+                for (int q = 0; q < k; ++q) {
+                    const int e = list[o + q];
+                    if ((e >> 7) == z) w = e & 127;
+                }
+                if (w < 0) { bad = true; break; }
+                const double wx = S.vx[w], wy = S.vy[w], wz = S.vz[w];
+                Ax += uy * wz - uz * wy;
+                Ay += uz * wx - ux * wz;
+                Az += ux * wy - uy * wx;
+                u = w; ux = wx; uy = wy; uz = wz;
+                ++steps;
+                if (u == u0 || steps >= k) break;
+            }
+            bad |= u != u0 || steps != k;  // not exactly one cycle through the face's k vertices
+        }
+        Ax *= 0.5; Ay *= 0.5; Az *= 0.5;
+        const double area = sqrt(Ax * Ax + Ay * Ay + Az * Az);
+        S.farea[f] = area;
+        const double4 pl = S.pl[f];
+        const double nn = pl.x * pl.x + pl.y * pl.y + pl.z * pl.z;
+        vol += (Ax * pl.x + Ay * pl.y + Az * pl.z) * pl.w / nn;
+        surf += area;
+    }
+    return bad;
+}
+
 // One warp's share of a cooperative job (warp w of T::WARPS; warp 0 is the cell's own warp).
 template <class T>
 __device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int lane) {
@@ -1591,9 +1691,8 @@ __device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int
                         const float sv = fmaf(D.x, v[u].x, fmaf(D.y, v[u].y, D.z * v[u].z)) - D.w;
                         if (sv > mk) cut |= 1u << k;
                         else if (fabsf(sv) <= mk && !((cut >> k) & 1u)) {
-                            const float D2 = fmaf(D.x, D.x, fmaf(D.y, D.y, D.z * D.z));
                             FPlane f;
-                            f.tl = 1e-12f * (D2 * rsqrtf(D2)) * c.rmax;
+                            f.nx = D.x; f.ny = D.y; f.nz = D.z; f.d = D.w; f.m = mk;
                             if (outside_fp64(c, J.csj[k], f, S.vx[sv_i], S.vy[sv_i], S.vz[sv_i])) cut |= 1u << k;
                         }
                     }
@@ -1718,6 +1817,12 @@ __device__ __noinline__ unsigned finalize(WarpState<T>& S, Cell& c, int lane, co
         }
         return 0u;
     }
+#ifdef PD_SKIP_FIN
+    if (!T::COOP && !T::GLOBAL) {  // EXPERIMENT ONLY: wrong output, measures the cell program without finalize
+        if (lane == 0) { O.cnt[i] = 0; O.aoff[i] = 0; O.vol[i] = 0.f; O.surf[i] = 0.f; O.flags[i] = 0; }
+        return 0u;
+    }
+#endif
     double vol = 0, surf = 0;
     if (T::COOP && c.nv >= P_coop_min_v(S)) {  // twins and faces over all warps of the CTA
         CoopJob& J = coop_job();
@@ -1729,6 +1834,11 @@ __device__ __noinline__ unsigned finalize(WarpState<T>& S, Cell& c, int lane, co
         for (int w = 0; w < T::WARPS; ++w) { vol += J.dpart[w][0]; surf += J.dpart[w][1]; missing |= J.ipart[w][0] != 0; }
         vol /= 3.0;
         if (missing && lane == 0) c.degraded = 1;
+    } else if (kFaceWalk<T>) {
+        const bool bad = areas_facewalk(S, c.nv, c.np, lane, vol, surf);
+        vol = warp_sum_d(vol) / 3.0;
+        surf = warp_sum_d(surf);
+        if (__any_sync(FULL, bad) && lane == 0) c.degraded = 1;
     } else if (kHashTwins<T>) {
         bool bad = twins_hash(S, c.nv, lane);
         bad |= areas_walk(S, c.nv, c.np, lane, vol, surf);
@@ -1804,6 +1914,88 @@ __device__ __noinline__ unsigned finalize(WarpState<T>& S, Cell& c, int lane, co
                                (degraded ? PD_CELL_DEGRADED : 0));
     }
     return min(ndrop, 0x7fffu) | (min(nsmall, 0x7fffu) << 15) | (degraded ? 1u << 30 : 0u);
+}
+
+// Deferred finalize (tier 1, CellParams::rec_*): store the finished cell's topology for finalize_kernel.
+template <class T>
+constexpr bool kDefer = std::is_same<T, Tier1>::value;  // finalize_kernel runs right after the tier-1 launch
+template <class T>
+__device__ __forceinline__ bool defer_cell(const WarpState<T>& S, const Cell& c, int lane, const CellParams& P, int s) {
+    const int nv = c.nv, np = c.np;
+    const unsigned words = 2u + (unsigned)np + (unsigned)nv;
+    unsigned long long off = 0;
+    if (lane == 0) off = atom_add_g(P.rec_top, words);
+    off = __shfl_sync(FULL, off, 0);
+    if (off + words > (unsigned long long)P.rec_cap) return false;  // arena full: finalize here
+    uint32_t* rec = P.rec_arena + off;
+    if (lane == 0) { rec[0] = (uint32_t)nv | ((uint32_t)np << 16); rec[1] = (uint32_t)c.degraded; }
+    for (int f = lane; f < np; f += 32) rec[2 + f] = (uint32_t)S.pid[f];
+    for (int u = lane; u < nv; u += 32) rec[2 + np + u] = (uint32_t)S.vt[u];
+    if (lane == 0) P.rec_index[s] = (uint32_t)off;
+    return true;
+}
+
+// Deferred finalize of tier 1: warp per recorded cell, Morton order.  The FP64 planes are rebuilt from the
+// neighbour ids exactly as the cell program built them (exact_plane / the walls of init_cell) and every vertex
+// by solve3 of its three planes -- the same function on the same operands, so the same values -- then the
+// same finalize() as in the cell kernel.
+template <class T>
+__global__ void __launch_bounds__(T::WARPS * 32) finalize_kernel(const __grid_constant__ CellParams P) {
+    const int lane = threadIdx.x & 31, wid = (int)(threadIdx.x >> 5);
+    WarpState<T>& S = reinterpret_cast<WarpState<T>*>(pd_smem)[wid];
+    Cell& c = S.c;
+    const int64_t gw = (int64_t)blockIdx.x * T::WARPS + wid, nw = (int64_t)gridDim.x * T::WARPS;
+    for (int64_t idx = gw; idx < P.count; idx += nw) {
+        const int s = (int)(P.begin + idx);
+        const uint32_t off = P.rec_index[s];
+        if (off == 0xffffffffu) continue;
+        const uint32_t* rec = P.rec_arena + off;
+        const uint32_t h0 = rec[0];
+        const int nv = (int)(h0 & 0xffffu), np = (int)(h0 >> 16);
+        const float4 site = __ldg(&P.sites[s]);
+        __syncwarp();
+        if (lane == 0) {
+            c.fpx = site.x; c.fpy = site.y; c.fpz = site.z; c.fpw = site.w;
+            c.px = site.x; c.py = site.y; c.pz = site.z; c.pw = site.w;
+            c.self = s;
+            c.self_orig = __ldg(&P.perm[s]);
+            c.nv = nv;
+            c.np = np;
+            c.degraded = (int)rec[1];
+        }
+        __syncwarp();
+        for (int f = lane; f < np; f += 32) {
+            const int pid = (int)rec[2 + f];
+            double4 pl;
+            if (pid < 0) {  // box wall k (init_cell)
+                const int k = -1 - pid, ax = k >> 1, pos = k & 1;
+                const double lo = (double)P.box_lo[ax] - (ax == 0 ? c.px : ax == 1 ? c.py : c.pz);
+                const double hi = (double)P.box_hi[ax] - (ax == 0 ? c.px : ax == 1 ? c.py : c.pz);
+                double n[3] = {0, 0, 0};
+                n[ax] = pos ? 1.0 : -1.0;
+                pl = make_double4(n[0], n[1], n[2], pos ? hi : -lo);
+            } else {
+                pl = exact_plane(c, __ldg(&P.sites[pid]));
+            }
+            S.pl[f] = pl;
+            S.pid[f] = pid;
+        }
+        __syncwarp();
+        for (int u = lane; u < nv; u += 32) {
+            const auto t = (typename T::trip_t)rec[2 + np + u];
+            double x, y, z;
+            solve3(S.pl, ta(t), tb(t), tc(t), x, y, z);
+            put_vertex(S.fv, S.vx, S.vy, S.vz, u, x, y, z);
+            S.vt[u] = t;
+        }
+        __syncwarp();
+        const unsigned rob = finalize(S, c, lane, P, ST_OK);
+        if (rob && lane == 0) {
+            red_add_g(&P.stats->dropped, rob & 0x7fffu);
+            red_add_g(&P.stats->small, (rob >> 15) & 0x7fffu);
+            red_add_g(&P.stats->degraded, rob >> 30);
+        }
+    }
 }
 
 __device__ __noinline__ void trace_print(int tier, const Cell& c, const Counters& a, const Counters& b, int st, long long cyc) {
@@ -1893,7 +2085,8 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(con
             }
             if (kStats<MODE> && st == ST_OVERFLOW) novf++;
             PT_BEGIN(t_fin);
-            const unsigned rob = finalize(S, c, lane, P, st);
+            const bool deferred = kDefer<T> && st == ST_OK && P.rec_index && defer_cell(S, c, lane, P, s);
+            const unsigned rob = deferred ? 0u : finalize(S, c, lane, P, st);
             if (rob && lane == 0) {  // robustness counters (rare, always published): straight to the device totals
                 red_add_g(&P.stats->dropped, rob & 0x7fffu);
                 red_add_g(&P.stats->small, (rob >> 15) & 0x7fffu);
@@ -1958,9 +2151,27 @@ cudaError_t launch_tier(const CellParams& p, int tier, cudaStream_t st, int num_
 
 }  // namespace
 
+cudaError_t launch_tier1(const CellParams& p, cudaStream_t st, int num_sms);
+
 cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches) {
     if (launches) ++*launches;
     if (tier == 0) {
+        cudaError_t e = launch_tier1(p, st, num_sms);
+        if (e != cudaSuccess || !p.rec_index) return e;
+        if (launches) ++*launches;
+        const size_t smem = sizeof(WarpState<Tier1>) * Tier1::WARPS;
+        cudaFuncSetAttribute(finalize_kernel<Tier1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, finalize_kernel<Tier1>, Tier1::WARPS * 32, smem);
+        finalize_kernel<Tier1><<<num_sms * (per_sm < 1 ? 1 : per_sm), Tier1::WARPS * 32, smem, st>>>(p);
+        return cudaGetLastError();
+    }
+    if (tier == 1) return launch_tier<Tier2, kDynMode>(p, 1, st, num_sms);
+    return launch_tier<Tier3, kDynMode>(p, 2, st, num_sms);
+}
+
+cudaError_t launch_tier1(const CellParams& p, cudaStream_t st, int num_sms) {
+    {
         // tier 1: specialized kernels for the common modes, each with and without the pd_stats counters
         constexpr unsigned S = PD_STATS;
         switch (p.flags & (kModeBits | PD_STATS)) {
@@ -1977,8 +2188,6 @@ cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num
             default: return launch_tier<Tier1, kDynMode>(p, 0, st, num_sms);
         }
     }
-    if (tier == 1) return launch_tier<Tier2, kDynMode>(p, 1, st, num_sms);
-    return launch_tier<Tier3, kDynMode>(p, 2, st, num_sms);
 }
 
 size_t cells_global_state_bytes(int num_sms) {

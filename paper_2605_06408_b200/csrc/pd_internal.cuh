@@ -91,6 +91,14 @@ struct CellParams {
     int start_tier;     // test knob ($PD_START_TIER): cells skip the tiers below it (default 0)
     int coop_min_v;     // top tier: vertex count from which O(V) passes use the whole CTA ($PD_COOP_MIN_V)
     int trace_cell;     // debug ($PD_TRACE_CELL): print the work counters of this original id (-1 = none)
+    // Deferred finalize (tier 1): the cell program stores each finished cell's topology -- its planes as
+    // neighbour ids and its vertices as plane-index triplets -- and a separate kernel rebuilds the FP64 planes
+    // and vertices from it and computes faces, areas and volume (keeps the finalize code out of the cell
+    // program's instruction-cache working set).  rec_index == NULL: finalize in the cell kernel.
+    uint32_t* rec_index;           // per Morton position: word offset of its record, ~0u = not deferred
+    uint32_t* rec_arena;           // records: [nv | np << 16, degraded, pid[np], vt[nv]]
+    unsigned long long* rec_top;   // bump pointer (words)
+    int64_t rec_cap;               // words (< 2^32); a cell that does not fit is finalized in the cell kernel
 };
 
 cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches);
