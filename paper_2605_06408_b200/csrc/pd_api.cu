@@ -526,6 +526,14 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         // ---- optional KNN warm start: K = 8 nearest sites of every site of the slice
         int32_t* knn = nullptr;
         Ev kev[2];
+        // auto warm start (pd.h PD_NO_AUTO_WARM): the sampled share of dominated sites decides; every rank of a
+        // sharded build samples the same broadcast sites, so all take the same decision
+        double dom_share = 0.0;
+        if (!(opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE | PD_NO_AUTO_WARM)) && n >= 1024 && (weights || comm)) {
+            unsigned long long* dcount = W.alloc<unsigned long long>(1);
+            ck(pd::dominated_share(sorted, n, dcount, &dom_share, st, &launches));
+            if (dom_share >= 0.2) opt.flags |= PD_WARM_START;
+        }
         if (opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE)) {
             knn = W.alloc<int32_t>((size_t)n * pd::KNN_K);
             kev[0].create();
@@ -817,6 +825,8 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         s.faces_dropped = (int64_t)hs.dropped;
         s.faces_near_degenerate = (int64_t)hs.small;
         s.degraded_cells = (int64_t)hs.degraded;
+        s.dominated_share = dom_share;
+        s.warm_start = (opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE)) ? 1 : 0;
         s.nnz = nnz;
         s.ms_bvh = t01;
         s.ms_cells = t12;

@@ -52,6 +52,7 @@ for cfg in a.configs:
                       "per_cell": {k: round(s[k] / n, 2) for k in ("nodes_visited", "leaves_visited", "sites_tested",
                                                                    "clip_tests", "clips")},
                       "tier_cells": s["tier_cells"], "dropped": s["faces_dropped"],
-                      "near_degenerate": s["faces_near_degenerate"], "degraded": s["degraded_cells"]}), flush=True)
+                      "near_degenerate": s["faces_near_degenerate"], "degraded": s["degraded_cells"],
+                      "dominated_share": round(s["dominated_share"], 4), "warm": s["warm_start"]}), flush=True)
     del d, p, w
     torch.cuda.empty_cache()

@@ -7,7 +7,7 @@ import csv
 import re
 import sys
 
-src = open("paper_2605_06408_b200/csrc/pd_cells.cu").read().split("\n")
+src = open(sys.argv[3] if len(sys.argv) > 3 else "paper_2605_06408_b200/csrc/pd_cells.cu").read().split("\n")
 starts = []
 fdef = re.compile(r"^(?:template <[^>]*>\s*)?(?:__device__|__global__)[^;(]*?\b(\w+)\s*\(")
 for i, line in enumerate(src, 1):
