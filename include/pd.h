@@ -74,11 +74,13 @@ enum {
     PD_TETS = 1u << 11,       /* also output the dual tetrahedra (the "explicit mesh"
                                  of PAPER.md:343/398): see pd_tets.  Not with shard_world > 1 (PD_EINVAL). */
     PD_NO_AUTO_WARM = 1u << 13 /* never switch the KNN warm start on by itself.  Default: with weights and neither
-                                  PD_WARM_START nor PD_WARM_ADAPTIVE given, a 64k-site sample measures the share of
-                                  sites inside a Morton neighbour's power ball (w_j - w_i > |p_j - p_i|^2, i.e. squeezed
-                                  or EMPTY cells) and PD_WARM_START is used when it is >= 20%
-                                  (heavy-tailed weights: C5 1.38 s with it vs 2.50 s without; light weights: C4 0.40 s
-                                  without vs 0.55 s with).  Correctness-neutral: the same diagram either way. */
+                                  PD_WARM_START nor PD_WARM_ADAPTIVE given, the tier-1 cell program runs on a strided
+                                  8k-site sample with and without the KNN pre-clip (deterministic per-cell work
+                                  counters, PD_COST) and PD_WARM_START is used when sampled work with it (x 1.10, plus
+                                  ~60 units per site for the KNN query) is below 0.9 x the work without
+                                  (pd_stats.warm_gain).  Costs two sample launches + one sync (~5 ms); every rank of
+                                  a sharded build measures the same sample and takes the same decision.  The diagram
+                                  is the same either way (areas/volumes to rounding). */
 };
 
 /* pd_cell_flags values */
@@ -125,7 +127,7 @@ typedef struct {
                                       (reading R2) */
     int64_t faces_near_degenerate; /* reported neighbour faces with area < 1e-9 S_i (the parity excusal band) */
     int64_t degraded_cells;        /* cells flagged PD_CELL_DEGRADED */
-    double dominated_share;        /* auto warm start: the sampled share (0 when not sampled) */
+    double warm_gain;              /* auto warm start: sampled work ratio with / without it (0 when not sampled) */
     int64_t warm_start;            /* 1 if the KNN warm start ran (given or switched on automatically) */
 } pd_stats;
 

@@ -60,7 +60,7 @@ class Stats(ctypes.Structure):
                 ("ms_total", ctypes.c_double), ("ms_tier", ctypes.c_double * 3),
                 ("warp_cycles", ctypes.c_int64 * 10), ("ms_knn", ctypes.c_double),
                 ("faces_dropped", ctypes.c_int64), ("faces_near_degenerate", ctypes.c_int64),
-                ("degraded_cells", ctypes.c_int64), ("dominated_share", ctypes.c_double), ("warm_start", ctypes.c_int64)]
+                ("degraded_cells", ctypes.c_int64), ("warm_gain", ctypes.c_double), ("warm_start", ctypes.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}

@@ -456,17 +456,12 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         // PD_BALANCE cuts equal estimated cost, from the tier-1 kernel's per-cell work counters on a
         // strided ~40k-cell sample (deterministic, so every rank computes the same cuts).  Measured on
         // C4 at world 8 (tools/shard_balance.py): equal-count max/mean 1.07, cost-balanced 1.16.
-        std::vector<int64_t> cuts(world + 1);  // every rank's slice (the exchange needs them all)
-        for (int q = 0; q <= world; ++q) cuts[q] = (n * q) / world;
-        if (world > 1 && (opt.flags & PD_BALANCE) && n >= 4 * world) {
-            const int64_t stride = std::max<int64_t>(1, n / 40000);
-            const int64_t ns = (n + stride - 1) / stride;
-            std::vector<int32_t> hpos(ns);
-            for (int64_t k = 0; k < ns; ++k) hpos[k] = (int32_t)(k * stride);
-            int32_t* spos = W.alloc<int32_t>(ns);
-            int32_t* scount = W.alloc<int32_t>(4);
+        // Sampled tier-1 work (deterministic per-cell counters nodes + sites + 8 x clips, PD_COST) of the listed
+        // Morton positions, run in list mode with scratch outputs: the cost model of PD_BALANCE's cuts and of the
+        // auto warm start.  Every rank of a sharded build runs it on the same broadcast sites, so all agree.
+        auto sample_work = [&](const int32_t* spos, int32_t* scount, int64_t ns, unsigned flags, const int32_t* sknn,
+                               int32_t* sgath) {
             int32_t* scost = W.alloc<int32_t>(n);
-            int32_t* sgath = W.alloc<int32_t>(ns);
             unsigned long long* sctr = W.alloc<unsigned long long>(8);
             const int64_t scap = ns * 96 + 4096;
             int32_t* s_nbr = W.alloc<int32_t>(scap);
@@ -475,7 +470,6 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             pd::Stats* s_stats = W.alloc<pd::Stats>(1);
             int32_t* s_next = W.alloc<int32_t>(ns);
             int32_t hc[4] = {(int32_t)ns, 0, 0, 0};
-            ck(cudaMemcpyAsync(spos, hpos.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, st));
             ck(cudaMemcpyAsync(scount, hc, sizeof(hc), cudaMemcpyHostToDevice, st));
             ck(cudaMemsetAsync(sctr, 0, 8 * sizeof(unsigned long long), st));
             ck(cudaMemsetAsync(s_ovf, 0, sizeof(int), st));
@@ -486,8 +480,9 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             Q.nodes = bvh.nodes;
             Q.root = bvh.root;
             for (int k = 0; k < 3; ++k) { Q.box_lo[k] = hbox[k]; Q.box_hi[k] = hbox[3 + k]; }
-            Q.flags = (opt.flags | PD_COST) & ~PD_STATS;
-            Q.out.cnt = cnt; Q.out.aoff = aoff; Q.out.vol = vol; Q.out.surf = surf; Q.out.flags = flags;
+            Q.flags = (flags | PD_COST) & ~PD_STATS;
+            Q.out.cnt = W.alloc<int32_t>(n); Q.out.aoff = W.alloc<int64_t>(n); Q.out.vol = W.alloc<float>(n);
+            Q.out.surf = W.alloc<float>(n); Q.out.flags = W.alloc<uint8_t>(n);
             Q.out.arena_nbr = s_nbr; Q.out.arena_area = s_area; Q.out.arena_top = sctr + 4;
             Q.out.arena_cap = scap; Q.out.arena_overflow = s_ovf; Q.out.cost = scost;
             Q.stats = s_stats;
@@ -497,6 +492,8 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             Q.prof_tier = -2;
             Q.coop_min_v = 128;
             Q.trace_cell = -1;
+            Q.knn = sknn;
+            Q.n_sites = n;
             Q.work_counter = sctr;
             Q.last_tier = 1;  // heavy sampled cells keep their (partial) cost instead of escalating
             Q.list = spos;
@@ -506,6 +503,50 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             Q.spill_cap = spill_cap[0];
             ck(pd::launch_cells(0, Q, st, sms, &launches));
             ck(pd::gather_sample_cost(perm, spos, ns, scost, sgath, st, &launches));
+        };
+        auto strided_sample = [&](int64_t target, int64_t& ns, int64_t& stride) {
+            stride = std::max<int64_t>(1, n / target);
+            ns = (n + stride - 1) / stride;
+            std::vector<int32_t> hpos(ns);
+            for (int64_t k = 0; k < ns; ++k) hpos[k] = (int32_t)(k * stride);
+            int32_t* spos = W.alloc<int32_t>(ns);
+            ck(cudaMemcpyAsync(spos, hpos.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, st));
+            ck(cudaStreamSynchronize(st));  // hpos is a host temporary
+            return spos;
+        };
+        // ---- auto warm start (pd.h PD_NO_AUTO_WARM): measure the sampled tier-1 work with and without the KNN
+        // pre-clip and keep it when it saves more than the KNN query costs
+        double warm_gain = 0.0;
+        int32_t* knn = nullptr;
+        if (!(opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE | PD_NO_AUTO_WARM)) && n >= 4096 && (weights || comm)) {
+            int64_t ns = 0, stride = 1;
+            const int32_t* spos = strided_sample(8192, ns, stride);
+            int32_t* scount = W.alloc<int32_t>(4);
+            knn = W.alloc<int32_t>((size_t)n * pd::KNN_K);
+            ck(pd::knn_query(sorted, bvh.nodes, bvh.root, 0, (int)ns, 0, knn, sms, st, &launches, spos));
+            int32_t* g0 = W.alloc<int32_t>(ns);
+            int32_t* g1 = W.alloc<int32_t>(ns);
+            sample_work(spos, scount, ns, opt.flags & ~(PD_WARM_START | PD_WARM_ADAPTIVE), nullptr, g0);
+            sample_work(spos, scount, ns, opt.flags | PD_WARM_START, knn, g1);
+            std::vector<int32_t> h0(ns), h1(ns);
+            ck(cudaMemcpyAsync(h0.data(), g0, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, st));
+            ck(cudaMemcpyAsync(h1.data(), g1, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, st));
+            ck(cudaStreamSynchronize(st));
+            double w0 = 0, w1 = 0;
+            for (int64_t k = 0; k < ns; ++k) { w0 += h0[k]; w1 += h1[k]; }
+            // the KNN query of a site costs about kKnnWork work units, and the warm-start kernel a few % more per unit
+            constexpr double kKnnWork = 60.0, kWarmOverhead = 1.10;
+            warm_gain = w0 > 0 ? (w1 * kWarmOverhead + kKnnWork * (double)ns) / w0 : 1.0;
+            if (warm_gain < 0.9) opt.flags |= PD_WARM_START;
+        }
+        std::vector<int64_t> cuts(world + 1);  // every rank's slice (the exchange needs them all)
+        for (int q = 0; q <= world; ++q) cuts[q] = (n * q) / world;
+        if (world > 1 && (opt.flags & PD_BALANCE) && n >= 4 * world) {
+            int64_t ns = 0, stride = 1;
+            const int32_t* spos = strided_sample(40000, ns, stride);
+            int32_t* scount = W.alloc<int32_t>(4);
+            int32_t* sgath = W.alloc<int32_t>(ns);
+            sample_work(spos, scount, ns, opt.flags & ~(PD_WARM_START | PD_WARM_ADAPTIVE), nullptr, sgath);
             std::vector<int32_t> hcost(ns);
             ck(cudaMemcpyAsync(hcost.data(), sgath, sizeof(int32_t) * ns, cudaMemcpyDeviceToHost, st));
             ck(cudaStreamSynchronize(st));
@@ -524,18 +565,9 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         r->slice_begin = begin;
         r->slice_end = end;
         // ---- optional KNN warm start: K = 8 nearest sites of every site of the slice
-        int32_t* knn = nullptr;
         Ev kev[2];
-        // auto warm start (pd.h PD_NO_AUTO_WARM): the sampled share of dominated sites decides; every rank of a
-        // sharded build samples the same broadcast sites, so all take the same decision
-        double dom_share = 0.0;
-        if (!(opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE | PD_NO_AUTO_WARM)) && n >= 1024 && (weights || comm)) {
-            unsigned long long* dcount = W.alloc<unsigned long long>(1);
-            ck(pd::dominated_share(sorted, n, dcount, &dom_share, st, &launches));
-            if (dom_share >= 0.2) opt.flags |= PD_WARM_START;
-        }
         if (opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE)) {
-            knn = W.alloc<int32_t>((size_t)n * pd::KNN_K);
+            if (!knn) knn = W.alloc<int32_t>((size_t)n * pd::KNN_K);
             kev[0].create();
             kev[1].create();
             ck(cudaEventRecord(kev[0], st));
@@ -825,7 +857,7 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         s.faces_dropped = (int64_t)hs.dropped;
         s.faces_near_degenerate = (int64_t)hs.small;
         s.degraded_cells = (int64_t)hs.degraded;
-        s.dominated_share = dom_share;
+        s.warm_gain = warm_gain;
         s.warm_start = (opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE)) ? 1 : 0;
         s.nnz = nnz;
         s.ms_bvh = t01;

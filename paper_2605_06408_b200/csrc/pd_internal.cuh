@@ -104,13 +104,11 @@ struct CellParams {
 cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches);
 int cells_grid_warps(int tier, int num_sms);
 size_t cells_global_state_bytes(int num_sms);
-// share of sampled sites dominated by a Morton neighbour's power ball (auto warm start); synchronizes `st`
-cudaError_t dominated_share(const float4* sites, int64_t n, unsigned long long* dcount, double* share, cudaStream_t st,
-                            int* launches);
 constexpr int KNN_K = 8;  // warm-start neighbours per site
 // K nearest sites (Euclidean, coincident sites excluded) of the Morton positions [begin, end) -> knn[s*K + k]
 // adaptive != 0: only sites dominated at their own position by their power-nearest neighbour keep a list
+// list != NULL: the positions list[begin..end) instead of the Morton range [begin, end)
 cudaError_t knn_query(const float4* sites, const WideNode* nodes, const NodeChild* root, int begin, int end, int adaptive,
-                      int32_t* knn, int num_sms, cudaStream_t st, int* launches);
+                      int32_t* knn, int num_sms, cudaStream_t st, int* launches, const int32_t* list = nullptr);
 
 }  // namespace pd

@@ -38,13 +38,14 @@ __device__ __forceinline__ int fordk(float f) {
 
 __global__ void __launch_bounds__(KNN_WARPS * 32) k_knn(const float4* __restrict__ sites, const WideNode* __restrict__ nodes,
                                                         const NodeChild* __restrict__ root, int begin, int end, int adaptive,
-                                                        int32_t* __restrict__ knn) {
+                                                        int32_t* __restrict__ knn, const int32_t* __restrict__ list) {
     __shared__ int st_node[KNN_WARPS][KNN_STACK];
     __shared__ float st_d[KNN_WARPS][KNN_STACK];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int gw = blockIdx.x * KNN_WARPS + wid, nw = gridDim.x * KNN_WARPS;
     const int root_link = __float_as_int(__ldg(&root->hi_l.w));
-    for (int s = begin + gw; s < end; s += nw) {
+    for (int it = begin + gw; it < end; it += nw) {
+        const int s = list ? __ldg(&list[it]) : it;  // a Morton range, or the listed positions list[begin..end)
         const float4 p = __ldg(&sites[s]);
         float bd = INFINITY;  // lanes 0..K-1: sorted K best squared distances
         int bi = -1;
@@ -123,53 +124,15 @@ __global__ void __launch_bounds__(KNN_WARPS * 32) k_knn(const float4* __restrict
     }
 }
 
-// Share of sites dominated by a nearby heavier site (auto warm start): sample every
-// `stride`-th Morton position s, count it when a Morton neighbour j (|j - s| <= 8; Morton neighbours are spatial
-// neighbours) has w_j - w_s > |p_j - p_s|^2, i.e. pi_j(p_s) < -w_s: p_s lies inside j's power ball and its own
-// cell is squeezed or empty.  A heuristic statistic (it only selects the work order), FP32.
-__global__ void k_dominated_sample(const float4* __restrict__ sites, int64_t n, int64_t stride, int64_t ns,
-                                   unsigned long long* __restrict__ count) {
-    unsigned c = 0;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < ns; k += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = k * stride;
-        const float4 p = __ldg(&sites[s]);
-        bool dom = false;
-        for (int d = -8; d <= 8 && !dom; ++d) {
-            const int64_t j = s + d;
-            if (d == 0 || j < 0 || j >= n) continue;
-            const float4 q = __ldg(&sites[j]);
-            const float dx = q.x - p.x, dy = q.y - p.y, dz = q.z - p.z;
-            dom = q.w - p.w > dx * dx + dy * dy + dz * dz;
-        }
-        c += dom ? 1u : 0u;
-    }
-    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
-}
-
 }  // namespace
 
-cudaError_t dominated_share(const float4* sites, int64_t n, unsigned long long* dcount, double* share, cudaStream_t st,
-                            int* launches) {
-    const int64_t ns = n < 65536 ? n : 65536;
-    const int64_t stride = ns > 0 ? n / ns : 1;
-    cudaMemsetAsync(dcount, 0, sizeof(unsigned long long), st);
-    if (launches) ++*launches;
-    k_dominated_sample<<<64, 256, 0, st>>>(sites, n, stride, ns, dcount);
-    unsigned long long h = 0;
-    cudaMemcpyAsync(&h, dcount, sizeof(h), cudaMemcpyDeviceToHost, st);
-    cudaError_t e = cudaStreamSynchronize(st);
-    *share = ns > 0 ? (double)h / (double)ns : 0.0;
-    return e != cudaSuccess ? e : cudaGetLastError();
-}
-
 cudaError_t knn_query(const float4* sites, const WideNode* nodes, const NodeChild* root, int begin, int end, int adaptive,
-                      int32_t* knn, int num_sms, cudaStream_t st, int* launches) {
+                      int32_t* knn, int num_sms, cudaStream_t st, int* launches, const int32_t* list) {
     if (end <= begin) return cudaSuccess;
     int grid = num_sms * 16;
     int need = (end - begin + KNN_WARPS - 1) / KNN_WARPS;
     if (grid > need) grid = need;
-    k_knn<<<grid, KNN_WARPS * 32, 0, st>>>(sites, nodes, root, begin, end, adaptive, knn);
+    k_knn<<<grid, KNN_WARPS * 32, 0, st>>>(sites, nodes, root, begin, end, adaptive, knn, list);
     if (launches) ++*launches;
     return cudaGetLastError();
 }

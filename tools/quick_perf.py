@@ -20,6 +20,7 @@ ap.add_argument("configs", nargs="*", default=["C4"])
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--leaf", type=int, default=0)
 a = ap.parse_args()
 pd.load_library()
 flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
@@ -28,7 +29,7 @@ for cfg in a.configs:
     p = torch.from_numpy(wl.points).cuda()
     w = None if wl.weights is None else torch.from_numpy(wl.weights).cuda()
     for _ in range(2):
-        d = pd.build_diagram(p, w, wl.box, flags=a.flags)
+        d = pd.build_diagram(p, w, wl.box, flags=a.flags, leaf_size=a.leaf)
         del d
     ms, tiers = [], []
     for _ in range(a.reps):
@@ -36,13 +37,13 @@ for cfg in a.configs:
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        d = pd.build_diagram(p, w, wl.box, flags=a.flags)
+        d = pd.build_diagram(p, w, wl.box, flags=a.flags, leaf_size=a.leaf)
         e1.record()
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
         tiers.append(d.stats["ms_tier"])
         del d
-    d = pd.build_diagram(p, w, wl.box, flags=a.flags | pd.STATS)
+    d = pd.build_diagram(p, w, wl.box, flags=a.flags | pd.STATS, leaf_size=a.leaf)
     s = d.stats
     n = wl.n
     print(json.dumps({"config": cfg, "n": n, "ms": round(float(np.mean(ms)), 2), "ms_min": round(min(ms), 2),
@@ -53,6 +54,6 @@ for cfg in a.configs:
                                                                    "clip_tests", "clips")},
                       "tier_cells": s["tier_cells"], "dropped": s["faces_dropped"],
                       "near_degenerate": s["faces_near_degenerate"], "degraded": s["degraded_cells"],
-                      "dominated_share": round(s["dominated_share"], 4), "warm": s["warm_start"]}), flush=True)
+                      "warm_gain": round(s["warm_gain"], 4), "warm": s["warm_start"]}), flush=True)
     del d, p, w
     torch.cuda.empty_cache()
