@@ -1342,9 +1342,28 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
     if (T::SPHERE) {
         c.flo[0] = c.flo[1] = c.flo[2] = 0.f;
         c.fhi[0] = c.fhi[1] = c.fhi[2] = 0.f;
+        __syncwarp();
+        update_aabb(S, c, lane);
+        return;
+    }
+    // the AABB of the box's corners: what update_aabb computes from their FP32 copies, without the warp reductions
+    // (keeps the once-per-cell code small: it shares the instruction cache with the hot loop)
+    float rm2 = 0.f, vm = 0.f, flo[3], fhi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        flo[k] = (float)lo[k];
+        fhi[k] = (float)hi[k];
+        flo[k] -= fabsf(flo[k]) * 2.4e-7f + 1e-30f;
+        fhi[k] += fabsf(fhi[k]) * 2.4e-7f + 1e-30f;
+        rm2 += fmaxf(flo[k] * flo[k], fhi[k] * fhi[k]);
+        vm = fmaxf(vm, fmaxf(-flo[k], fhi[k]));
     }
     __syncwarp();
-    update_aabb(S, c, lane);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { c.flo[k] = flo[k]; c.fhi[k] = fhi[k]; }
+    c.rmax = sqrtf(rm2);
+    c.vmax = vm;
+    __syncwarp();
 }
 
 // Twins: the vertex across each directed edge of vertex u (slots u0, u0+stride, ...).
@@ -1526,9 +1545,13 @@ constexpr bool kFaceWalk = PD_FACE_WALK && T::PMAX <= 64 && T::VMAX <= 128 && !T
 
 template <class T>
 __device__ __forceinline__ bool areas_facewalk(WarpState<T>& S, int nv, int np, int lane, double& vol, double& surf) {
-    uint32_t* const off = S.fcnt;
-    uint32_t* const cur = S.ffill;
-    uint16_t* const list = S.flist;
+    uint32_t* const off = S.fcnt;   // per face: CSR offset of its entries
+    uint32_t* const cur = S.ffill;  // per face: entry count
+    // scratch in arrays the finalize does not read: the FP32 vertex copies hold the entries (u | y << 7 | f << 14:
+    // vertex u on face f, y = the plane after f in u's CCW triplet), tw the successor vertex of every entry and,
+    // per vertex, the entry index of each of its three faces
+    uint32_t* const ent = reinterpret_cast<uint32_t*>(S.fv);
+    uint16_t* const succ = &S.tw[0][0];
     for (int f = lane; f < np; f += 32) { off[f] = 0u; cur[f] = 0u; }
     __syncwarp();
     for (int u = lane; u < nv; u += 32) {
@@ -1552,42 +1575,66 @@ __device__ __forceinline__ bool areas_facewalk(WarpState<T>& S, int nv, int np, 
         if (f0 + 1 < np) off[f0 + 1] = inc - c1;
     }
     __syncwarp();
+    // fill; every vertex remembers the entry index of its faces a (in rem) and b, c (the halves of bnd)
     for (int u = lane; u < nv; u += 32) {
         const auto t = S.vt[u];
         const int a = ta(t), b = tb(t), cc = tc(t);
-        list[off[a] + atomicAdd(&cur[a], 1u)] = (uint16_t)(u | b << 7);   // on face a: (a, b, c), y = b
-        list[off[b] + atomicAdd(&cur[b], 1u)] = (uint16_t)(u | cc << 7);  // on face b: (b, c, a), y = c
-        list[off[cc] + atomicAdd(&cur[cc], 1u)] = (uint16_t)(u | a << 7); // on face c: (c, a, b), y = a
+        const uint32_t ea = off[a] + atomicAdd(&cur[a], 1u), eb = off[b] + atomicAdd(&cur[b], 1u),
+                       ec = off[cc] + atomicAdd(&cur[cc], 1u);
+        ent[ea] = (uint32_t)u | (uint32_t)b << 7 | (uint32_t)a << 14;   // on face a: (a, b, c), y = b
+        ent[eb] = (uint32_t)u | (uint32_t)cc << 7 | (uint32_t)b << 14;  // on face b: (b, c, a), y = c
+        ent[ec] = (uint32_t)u | (uint32_t)a << 7 | (uint32_t)cc << 14;  // on face c: (c, a, b), y = a
+        S.rem[u] = (uint16_t)ea;
+        S.bnd[u] = eb | ec << 16;
     }
     __syncwarp();
+    const int ne = 3 * nv;
     bool bad = false;
+    // successor of every entry (lane = entry): vertex u on face f, (f, y, z) rotated; its successor on f's loop is
+    // the entry of f whose y equals z (the holder of the reverse of u's dual edge z -> f)
+    for (int e = lane; e < ne; e += 32) {
+        const uint32_t x = ent[e];
+        const int u = (int)(x & 127u), f = (int)(x >> 14);
+        const auto t = S.vt[u];
+        const int a = ta(t), b = tb(t), cc = tc(t);
+        const int z = a == f ? cc : (b == f ? a : b);
+        const int o = (int)off[f], k = (int)cur[f];
+        int w = 0xffff;
+        for (int q = 0; q < k; ++q) {
+            const uint32_t y = ent[o + q];
+            if ((int)((y >> 7) & 127u) == z) w = (int)(y & 127u);
+        }
+        bad |= w == 0xffff;
+        succ[e] = (uint16_t)w;
+    }
+    __syncwarp();
+    // walk each face's loop (lane = face) from its lowest vertex slot: deterministic summation order
     for (int f = lane; f < np; f += 32) {
         const int o = (int)off[f], k = (int)cur[f];
         double Ax = 0, Ay = 0, Az = 0;
         if (k > 0) {
-            int u0 = 0x7fff;
-            for (int q = 0; q < k; ++q) u0 = min(u0, (int)(list[o + q] & 127u));
-            int u = u0, steps = 0;
+            int e0 = o;
+            for (int q = 1; q < k; ++q)
+                if ((ent[o + q] & 127u) < (ent[e0] & 127u)) e0 = o + q;
+            int e = e0, steps = 0;
+            int u = (int)(ent[e] & 127u);
             double ux = S.vx[u], uy = S.vy[u], uz = S.vz[u];
             for (;;) {
-                const auto t = S.vt[u];
-                const int a = ta(t), b = tb(t), cc = tc(t);
-                const int z = a == f ? cc : (b == f ? a : b);  // u's plane before f (CCW)
-                int w = -1;
-                for (int q = 0; q < k; ++q) {
-                    const int e = list[o + q];
-                    if ((e >> 7) == z) w = e & 127;
-                }
-                if (w < 0) { bad = true; break; }
+                const int w = succ[e];
+                if (w == 0xffff) { bad = true; break; }
                 const double wx = S.vx[w], wy = S.vy[w], wz = S.vz[w];
                 Ax += uy * wz - uz * wy;
                 Ay += uz * wx - ux * wz;
                 Az += ux * wy - uy * wx;
-                u = w; ux = wx; uy = wy; uz = wz;
                 ++steps;
-                if (u == u0 || steps >= k) break;
+                // w's entry on face f: its triplet slot holding f
+                const auto t = S.vt[w];
+                const uint32_t bc = S.bnd[w];
+                e = ta(t) == f ? (int)S.rem[w] : (tb(t) == f ? (int)(bc & 0xffffu) : (int)(bc >> 16));
+                u = w; ux = wx; uy = wy; uz = wz;
+                if (e == e0 || steps >= k) break;
             }
-            bad |= u != u0 || steps != k;  // not exactly one cycle through the face's k vertices
+            bad |= e != e0 || steps != k;  // not exactly one cycle through the face's k vertices
         }
         Ax *= 0.5; Ay *= 0.5; Az *= 0.5;
         const double area = sqrt(Ax * Ax + Ay * Ay + Az * Az);
