@@ -13,7 +13,7 @@ M=$M,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__issue_active.avg.pc
 M=$M,sm__cycles_elapsed.avg.per_second,smsp__sass_thread_inst_executed_op_fadd_pred_on.sum
 M=$M,smsp__sass_thread_inst_executed_op_fmul_pred_on.sum,smsp__sass_thread_inst_executed_op_ffma_pred_on.sum
 M=$M,smsp__thread_inst_executed_per_inst_executed.ratio,sm__inst_executed.avg.per_cycle_active
-ncu --metrics $M --clock-control none --kernel-name regex:cells_kernel -s 3 -c 3 --csv \
+ncu --metrics $M --clock-control none --kernel-name regex:"cells_kernel|finalize_kernel" -s 4 -c 4 --csv \
     --log-file gpurun_out/${R}_cells_traffic.csv python tools/prof_c4n.py > gpurun_out/${R}_traffic.log 2>&1
 ncu --set full --import-source on --clock-control none --kernel-name regex:cells_kernel -s 3 -c 1 \
     -o gpurun_out/${R}_cells_full_c4_1m python tools/prof_c4n.py 1000000 > gpurun_out/${R}_full.log 2>&1

@@ -56,7 +56,8 @@ T = read_ncu_csv(f"{G}/{R}_cells_traffic.csv")
 per = defaultdict(dict)
 for d in T:
     k = d["Kernel Name"]
-    tier = "tier1" if "TierCfg<96" in k else ("tier2" if "TierCfg<384" in k else "tier3")
+    tier = ("finalize" if "finalize_kernel" in k else "tier1" if "TierCfg<96" in k else
+            "tier2" if "TierCfg<384" in k else "tier3")
     per[tier][d["Metric Name"]] = (d["Metric Value"], d["Metric Unit"])
 t1 = per.get("tier1", {})
 rd = float(t1.get("dram__bytes_read.sum", ("0",))[0])
