@@ -599,9 +599,10 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         int64_t tcap = std::max<int64_t>((end - begin) * 8, 4096);
         // deferred tier-1 finalize (pd_cells.cu finalize_kernel): per-cell topology records, ~60 words per
         // cell on average (2 + planes + vertices); a cell that does not fit is finalized in the cell kernel
-        const bool defer = !getenv("PD_DEFER") || atoi(getenv("PD_DEFER")) != 0;
+        const bool defer = true;  // tier 1 keeps no FP64 vertices: its finalize always runs in finalize_kernel
         uint32_t* rec_index = defer ? W.alloc<uint32_t>((size_t)std::max<int64_t>(n, 1)) : nullptr;
-        const int64_t rec_cap = std::min<int64_t>(std::max<int64_t>((end - begin) * 80, 1 << 16), 0xfffffff0LL);
+        int64_t rec_cap = std::min<int64_t>(std::max<int64_t>((end - begin) * 80, 1 << 16), 0xfffffff0LL);
+        if (getenv("PD_REC_CAP")) rec_cap = std::max<int64_t>(atoll(getenv("PD_REC_CAP")), 16);  // test knob
         uint32_t* rec_arena = defer ? W.alloc<uint32_t>((size_t)rec_cap) : nullptr;
         for (int attempt = 0; attempt < 3; ++attempt) {
             anbr = W.alloc<int32_t>(cap);

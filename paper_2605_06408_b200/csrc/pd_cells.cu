@@ -73,9 +73,22 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PD_PRETEST
 #define PD_PRETEST 1  // per leaf: every candidate against every vertex at once (lane = vertex), FP32 only
 #endif
+#ifndef PD_REFILTER
+#define PD_REFILTER 0  // re-run the pre-test on a leaf's remaining candidates after each clip
+#endif
+#ifndef PD_REFILTER_MIN
+#define PD_REFILTER_MIN 2  // ... when at least this many remain
+#endif
+#ifndef PD_PRETEST_COMPACT
+#define PD_PRETEST_COMPACT 1  // the pre-test's candidate planes packed by rank (no empty groups of 4)
+#endif
 
-template <int V, int P, int Q, int W, int MINB, bool GLOB = false, bool CO = false, bool SPH = false>
+template <int V, int P, int Q, int W, int MINB, bool GLOB = false, bool CO = false, bool SPH = false, bool F64 = true>
 struct TierCfg {
+    // FP64 vertex copies in the state.  Tier 1 keeps none (its finalize is deferred to finalize_kernel, which
+    // rebuilds every vertex from its plane triplet): the rare FP64 certification of an ambiguous FP32
+    // classification re-solves the vertex from its three FP64 planes instead (same solve3, same operands).
+    static constexpr bool F64V = F64;
     static constexpr bool GLOBAL = GLOB;     // warp state in global memory (top tier) instead of smem
     // CTA-cooperative cell (top tier): warp 0 runs the cell program, warps 1..W-1 join its O(V) passes
     static constexpr bool COOP = CO;
@@ -112,7 +125,12 @@ struct TierCfg {
 #ifndef PD_T1_SPHERE
 #define PD_T1_SPHERE 0
 #endif
-using Tier1 = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, PD_T1_WARPS, PD_T1_MINB, false, false, PD_T1_SPHERE != 0>;
+#ifndef PD_T1_F64V
+#define PD_T1_F64V 0
+#endif
+using Tier1 = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, PD_T1_WARPS, PD_T1_MINB, false, false, PD_T1_SPHERE != 0, PD_T1_F64V != 0>;
+// the state finalize_kernel rebuilds a deferred tier-1 cell into (with the FP64 vertices finalize() reads)
+using Tier1F = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, PD_T1_WARPS, PD_T1_MINB, false, false, PD_T1_SPHERE != 0, true>;
 // Tier 2: one cell per CTA of 4 warps (state in shared memory, O(V) passes CTA-wide from 128 vertices):
 // the few heavy cells of a light-weight workload (C4: 78) no longer run on one warp each, which
 // mattered most for the per-rank critical path of sharded builds.
@@ -154,7 +172,7 @@ struct __align__(16) WarpState {
     Cell c;                       // warp-uniform cell state
     double4 pl[T::PMAX];          // plane n.y <= d (n = p_j - p_i, local coordinates), exact
     float4 fv[T::VMAX];           // FP32 copy of the vertex positions (x, y, z, 0)
-    double vx[T::VMAX], vy[T::VMAX], vz[T::VMAX];
+    double vx[T::F64V ? T::VMAX : 1], vy[T::F64V ? T::VMAX : 1], vz[T::F64V ? T::VMAX : 1];
     typename T::trip_t vt[T::VMAX];  // plane-index triplet (a, b, c), CCW seen from outside
     int32_t pid[T::PMAX];         // >= 0 Morton index of the neighbour site; -1-k box wall k
     union {
@@ -335,6 +353,9 @@ __device__ __forceinline__ float dir_r2(const Cell& c, unsigned allow, bool iso)
 //      so no plane of B cuts the cell if d^2 + w_i - w_max > 2H.  (2) is never looser than (1) for
 //      small far boxes (Cauchy-Schwarz) and is disabled by PD_PAPER_BOUND / PD_ISOTROPIC.
 // Returns the Alg. 1 priority delta = NodeSqrDist - r^2 (+ the weight term): order only.
+#ifndef PD_NODE_KEY
+#define PD_NODE_KEY 0  // default mode's queue priority: 0 Alg. 1's d^2 + min(0,dw) - r^2 (with bound (1)); 1 d^2 + min(0,dw)
+#endif
 __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi_l, unsigned flags, bool& culled) {
     const bool iso = (flags & PD_ISOTROPIC) != 0;
     const bool paper = (flags & (PD_PAPER_BOUND | PD_ISOTROPIC)) != 0;
@@ -342,6 +363,18 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
     float b0 = hi_l.x - c.fpx, b1 = hi_l.y - c.fpy, b2 = hi_l.z - c.fpz;
     float g0 = fmaxf(fmaxf(a0, -b0), 0.f), g1 = fmaxf(fmaxf(a1, -b1), 0.f), g2 = fmaxf(fmaxf(a2, -b2), 0.f);
     float d2 = g0 * g0 + g1 * g1 + g2 * g2;
+    if (PD_NODE_KEY == 1 && !paper) {
+        // the AABB-support bound (2) alone: it is the tighter one wherever a node is near the cell, and the
+        // paper's (1) costs a directional radius and a square root per node (culling only; output identical)
+        const float dw = c.fpw - lo_w.w;
+        const float h0 = fmaxf(fmaxf(c.flo[0] * a0, c.flo[0] * b0), fmaxf(c.fhi[0] * a0, c.fhi[0] * b0));
+        const float h1 = fmaxf(fmaxf(c.flo[1] * a1, c.flo[1] * b1), fmaxf(c.fhi[1] * a1, c.fhi[1] * b1));
+        const float h2 = fmaxf(fmaxf(c.flo[2] * a2, c.flo[2] * b2), fmaxf(c.fhi[2] * a2, c.fhi[2] * b2));
+        const float H = h0 + h1 + h2;
+        const float mag = c.vmax * (fmaxf(fabsf(a0), fabsf(b0)) + fmaxf(fabsf(a1), fabsf(b1)) + fmaxf(fabsf(a2), fabsf(b2)));
+        culled = d2 + dw - 2.f * H > 1e-5f * (d2 + fabsf(dw) + 2.f * mag);
+        return d2 + fminf(0.f, dw);
+    }
     unsigned allow = (b0 >= 0.f ? 1u : 0u) | (a0 <= 0.f ? 2u : 0u) | (b1 >= 0.f ? 4u : 0u) | (a1 <= 0.f ? 8u : 0u) |
                      (b2 >= 0.f ? 16u : 0u) | (a2 <= 0.f ? 32u : 0u);
     float dw = c.fpw - lo_w.w;
@@ -536,8 +569,10 @@ __device__ PD_INL_AABB void update_aabb(const WarpState<T>& S, Cell& c, int lane
     }
 }
 
-__device__ __forceinline__ void put_vertex(float4* fv, double* vx, double* vy, double* vz, int s, double x, double y, double z) {
-    vx[s] = x; vy[s] = y; vz[s] = z;
+template <class T>
+__device__ __forceinline__ void put_vertex(WarpState<T>& S, int s, double x, double y, double z) {
+    float4* fv = S.fv;
+    if (T::F64V) { S.vx[s] = x; S.vy[s] = y; S.vz[s] = z; }
     fv[s] = make_float4((float)x, (float)y, (float)z, 0.f);
 }
 
@@ -597,6 +632,18 @@ __device__ __forceinline__ void solve3(const double4* pl, int ia, int ib, int ic
     x *= inv; y *= inv; z *= inv;
 }
 
+// FP64 position of vertex slot s: the stored copy, or (tiers without FP64 copies) re-solved from its plane
+// triplet exactly as it was created (solve3 on the same FP64 planes: the same value; box corners are exact).
+template <class T>
+__device__ __forceinline__ void vertex64(const WarpState<T>& S, int s, double& x, double& y, double& z) {
+    if (T::F64V) {
+        x = S.vx[s]; y = S.vy[s]; z = S.vz[s];
+    } else {
+        const auto t = S.vt[s];
+        solve3(S.pl, ta(t), tb(t), tc(t), x, y, z);
+    }
+}
+
 // Clip the cell by {y : n.y <= d} (re-designed warp-parallel).
 __device__ __forceinline__ double4 exact_plane(const Cell& c, float4 sj) {
     // the exact FP64 plane of candidate site sj: n = p_j - p_i, d = (|n|^2 + w_i - w_j)/2
@@ -638,6 +685,20 @@ __device__ __forceinline__ bool outside_fp64(const Cell& c, float4 sj, const FPl
     return fma(pe.x, vx, fma(pe.y, vy, pe.z * vz)) - pe.w > (double)cert_tol(f, c.rmax);
 }
 
+// The FP64 certification of an ambiguous FP32 classification (rare).  Out of line in the tiers without FP64
+// vertex copies: re-solving the vertex must not add its FP64 registers to the inlined hot loop's pressure.
+template <class T>
+__device__ __noinline__ bool outside_cert_solve(const WarpState<T>& S, const Cell& c, float4 sj, FPlane f, int s) {
+    double x, y, z;
+    vertex64(S, s, x, y, z);
+    return outside_fp64(c, sj, f, x, y, z);
+}
+template <class T>
+__device__ __forceinline__ bool outside_cert(const WarpState<T>& S, const Cell& c, float4 sj, const FPlane& f, int s) {
+    if (T::F64V) return outside_fp64(c, sj, f, S.vx[s], S.vy[s], S.vz[s]);
+    return outside_cert_solve(S, c, sj, f, s);
+}
+
 template <class T>
 __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, FPlane f, int pidn, Counters& cnt) {
     PT_BEGIN(t_cls);
@@ -662,7 +723,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
             float4 v = S.fv[s];
             float s32 = fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d;
             if (fabsf(s32) > f.m) out = s32 > 0.f;
-            else out = outside_fp64(c, sj, f, S.vx[s], S.vy[s], S.vz[s]);
+            else out = outside_cert(S, c, sj, f, s);
             if (!out) box.add(v);
         }
         unsigned m = __ballot_sync(FULL, out);
@@ -796,7 +857,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
             double vx, vy, vz;
             solve3(S.pl, hs, x, y, vx, vy, vz);
             int slot = e < R ? S.rem[e] : nv0 + (e - R);
-            put_vertex(S.fv, S.vx, S.vy, S.vz, slot, vx, vy, vz);
+            put_vertex(S, slot, vx, vy, vz);
             S.vt[slot] = tpack<typename T::trip_t>(hs, x, y);
             box.add(make_float4((float)vx, (float)vy, (float)vz, 0.f));
         }
@@ -810,7 +871,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
             unsigned mm = __ballot_sync(FULL, mover);
             if (mover) {
                 int dst = S.rem[B + moved + __popc(mm & lanemask_lt())];
-                S.vx[dst] = S.vx[s]; S.vy[dst] = S.vy[s]; S.vz[dst] = S.vz[s];
+                if (T::F64V) { S.vx[dst] = S.vx[s]; S.vy[dst] = S.vy[s]; S.vz[dst] = S.vz[s]; }
                 S.fv[dst] = S.fv[s];
                 S.vt[dst] = S.vt[s];
             }
@@ -878,8 +939,11 @@ __device__ __noinline__ bool cuts_fp64(const WarpState<T>& S, const Cell& c, flo
     double ex = (double)sj.x - c.px, ey = (double)sj.y - c.py, ez = (double)sj.z - c.pz;
     double ed = 0.5 * (ex * ex + ey * ey + ez * ez + (c.pw - (double)sj.w));
     double tol = 1e-12 * (double)sqrtf(D2) * (double)c.rmax;
-    for (int k = 0; k < c.nv; ++k)
-        if (fma(ex, S.vx[k], fma(ey, S.vy[k], ez * S.vz[k])) - ed > tol) return true;
+    for (int k = 0; k < c.nv; ++k) {
+        double x, y, z;
+        vertex64(S, k, x, y, z);
+        if (fma(ex, x, fma(ey, y, ez * z)) - ed > tol) return true;
+    }
     return false;
 }
 
@@ -950,13 +1014,47 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
     float key = cand ? dd * rsqrtf(D2) : INFINITY;  // d_ij: nearest plane first
     // the candidates' planes wait in shared memory (lane = candidate), so that no per-candidate value but
     // the key stays in registers through clip()
-    if (cand) { S.cpl[lane] = make_float4(Dx, Dy, Dz, dd); S.cmg[lane] = m; }
+    // candidate planes stored by rank among the candidates (the pre-test runs over ceil(k/4) groups, no gaps)
+    const unsigned mask0 = mask;
+    const int ncand = __popc(mask0);
+    const int myslot = PD_PRETEST_COMPACT ? __popc(mask0 & lanemask_lt()) : lane;
+    if (cand) { S.cpl[myslot] = make_float4(Dx, Dy, Dz, dd); S.cmg[myslot] = m; }
+    if (PD_PRETEST_COMPACT && lane >= ncand && lane < ((ncand + 3) & ~3)) {  // the last group's padding
+        S.cpl[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        S.cmg[lane] = 0.f;
+    }
     __syncwarp();
-    if (PD_PRETEST && !batched) {
-        // Pre-test, lane = vertex, all candidates at once (independent FMA chains, groups of 4 planes in
-        // flight): bit k <=> candidate k has some FP32 value above -m_k on the CURRENT cell.  A candidate
-        // with none has every vertex strictly inside (|s32 - s| < m), i.e. the certified classification
-        // of clip() would remove nothing now or on any later (smaller) cell: dropped for good.
+    // Pre-test, lane = vertex, all candidates at once (independent FMA chains, groups of 4 planes in
+    // flight): bit k <=> candidate slot k has some FP32 value above -m_k on the CURRENT cell.  A candidate
+    // with none has every vertex strictly inside (|s32 - s| < m), i.e. the certified classification
+    // of clip() would remove nothing now or on any later (smaller) cell: dropped for good.  Run on the
+    // leaf's candidates, and again on the remaining ones after each clip (PD_REFILTER): most planes that cut
+    // the cell the leaf started with no longer cut it once the nearest have clipped.
+    auto pretest = [&](unsigned smask) -> unsigned {
+        unsigned hit = 0u;
+        const int nv0 = c.nv;
+        for (int sv = lane; sv - lane < nv0; sv += 32) {
+            const bool vin = sv < nv0;
+            const float4 v = vin ? S.fv[sv] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+            for (int k0 = 0; k0 < ncand; k0 += 4) {
+                if (!((smask >> k0) & 0xfu)) continue;
+                const float4 mg = *reinterpret_cast<const float4*>(&S.cmg[k0]);
+                const float4 p0 = S.cpl[k0], p1 = S.cpl[k0 + 1], p2 = S.cpl[k0 + 2], p3 = S.cpl[k0 + 3];
+                const bool h0 = fmaf(p0.x, v.x, fmaf(p0.y, v.y, p0.z * v.z)) - p0.w > -mg.x;
+                const bool h1 = fmaf(p1.x, v.x, fmaf(p1.y, v.y, p1.z * v.z)) - p1.w > -mg.y;
+                const bool h2 = fmaf(p2.x, v.x, fmaf(p2.y, v.y, p2.z * v.z)) - p2.w > -mg.z;
+                const bool h3 = fmaf(p3.x, v.x, fmaf(p3.y, v.y, p3.z * v.z)) - p3.w > -mg.w;
+                if (vin) hit |= ((h0 ? 1u : 0u) | (h1 ? 2u : 0u) | (h2 ? 4u : 0u) | (h3 ? 8u : 0u)) << k0;
+            }
+        }
+        return __reduce_or_sync(FULL, hit);
+    };
+    if (PD_PRETEST && PD_PRETEST_COMPACT && !batched) {
+        const unsigned hr = pretest(ncand == 32 ? FULL : (1u << ncand) - 1u);
+        cand = cand && ((hr >> myslot) & 1u);
+        mask = __ballot_sync(FULL, cand);
+    } else if (PD_PRETEST && !batched) {  // candidates stored by lane (PD_PRETEST_COMPACT=0)
         unsigned hit = 0u;
         const int nv0 = c.nv;
         for (int sv = lane; sv - lane < nv0; sv += 32) {
@@ -964,8 +1062,7 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
             const float4 v = vin ? S.fv[sv] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
             for (int k0 = 0; k0 < 32; k0 += 4) {
-                const unsigned g = (mask >> k0) & 0xfu;
-                if (!g) continue;
+                if (!((mask >> k0) & 0xfu)) continue;
                 const float4 mg = *reinterpret_cast<const float4*>(&S.cmg[k0]);
                 const float4 p0 = S.cpl[k0], p1 = S.cpl[k0 + 1], p2 = S.cpl[k0 + 2], p3 = S.cpl[k0 + 3];
                 const bool h0 = fmaf(p0.x, v.x, fmaf(p0.y, v.y, p0.z * v.z)) - p0.w > -mg.x;
@@ -989,9 +1086,10 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         // would remove nothing: such a plane never cuts this or any later (smaller) cell.
         FPlane f;
         {
-            const float4 pl = S.cpl[src];
+            const int sl = PD_PRETEST_COMPACT ? __popc(mask0 & ((1u << src) - 1u)) : src;
+            const float4 pl = S.cpl[sl];
             f.nx = pl.x; f.ny = pl.y; f.nz = pl.z; f.d = pl.w;
-            f.m = S.cmg[src];
+            f.m = S.cmg[sl];
         }
         if (PD_FAST_REJECT) {
             const int nv0 = c.nv;
@@ -1008,6 +1106,9 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         const int jsrc = __shfl_sync(FULL, j, src);
         const float4 sjs = __ldg(&P.sites[jsrc]);  // the site itself (FP64 plane of the certification)
         PT_BEGIN(t_clip);
+#ifdef PD_COUNT_CALLS  // measurement build: clip() calls counted in the queue-spill counter
+        if (kStats<MODE>) cnt.spills++;
+#endif
         int st = clip(S, c, lane, sjs, f, jsrc, cnt);
         PT_END(t_clip, 3);
         if (st == CLIP_EMPTY) return ST_EMPTY;
@@ -1015,7 +1116,13 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         if (st == CLIP_DONE) {
             if (kStats<MODE>) cnt.clips++;
             cnt.work += 8;
-            if (cand && site_culled_pl<T::SPHERE>(c, S.cpl[lane], flags)) cand = false;
+            if (cand && site_culled_pl<T::SPHERE>(c, S.cpl[myslot], flags)) cand = false;
+            if (PD_REFILTER && PD_PRETEST_COMPACT && !batched) {
+                if (__popc(__ballot_sync(FULL, cand)) >= PD_REFILTER_MIN) {
+                    const unsigned hr = pretest(__reduce_or_sync(FULL, cand ? 1u << myslot : 0u));
+                    cand = cand && ((hr >> myslot) & 1u);
+                }
+            }
         }
         mask = __ballot_sync(FULL, cand);
     }
@@ -1330,7 +1437,7 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
     }
     if (lane < 8) {
         int sx = lane & 1, sy = (lane >> 1) & 1, sz = (lane >> 2) & 1;
-        put_vertex(S.fv, S.vx, S.vy, S.vz, lane, sx ? hi[0] : lo[0], sy ? hi[1] : lo[1], sz ? hi[2] : lo[2]);
+        put_vertex(S, lane, sx ? hi[0] : lo[0], sy ? hi[1] : lo[1], sz ? hi[2] : lo[2]);
         int X = sx, Y = 2 + sy, Z = 4 + sz;
         int sgn = (sx ? 1 : -1) * (sy ? 1 : -1) * (sz ? 1 : -1);  // det of the outward normals
         S.vt[lane] = sgn > 0 ? tpack<typename T::trip_t>(X, Y, Z) : tpack<typename T::trip_t>(X, Z, Y);
@@ -1848,20 +1955,27 @@ __device__ __noinline__ void emit_tets(WarpState<T>& S, const Cell& c, int lane,
 // Returns the cell's robustness counts packed: faces dropped (bits 0-14), near-degenerate neighbour faces
 // (bits 15-29), degraded (bit 30) -- returned rather than added to the caller's Counters, which would
 // otherwise have its address taken by this out-of-line call and live on the thread stack.
+// The per-cell output of a cell without a polytope (EMPTY, DUPLICATE, or OVERFLOW in the last tier).
+__device__ __forceinline__ void finalize_status(const Cell& c, int lane, const CellParams& P, int status) {
+    const int i = c.self_orig;
+    const CellOut& O = P.out;
+    if (lane == 0) {
+        if (O.tarena) { O.tcnt[i] = 0; O.taoff[i] = 0; }
+        O.cnt[i] = 0;
+        O.aoff[i] = 0;
+        O.vol[i] = 0.f;
+        O.surf[i] = 0.f;
+        O.flags[i] = (uint8_t)(status == ST_OVERFLOW ? PD_CELL_OVERFLOW
+                                                     : (PD_CELL_EMPTY | (status == ST_DUP ? PD_CELL_DUPLICATE : 0)));
+    }
+}
+
 template <class T>
 __device__ __noinline__ unsigned finalize(WarpState<T>& S, Cell& c, int lane, const CellParams& P, int status) {
     const int i = c.self_orig;
     const CellOut& O = P.out;
     if (status == ST_EMPTY || status == ST_DUP || status == ST_OVERFLOW) {
-        if (lane == 0) {
-            if (O.tarena) { O.tcnt[i] = 0; O.taoff[i] = 0; }
-            O.cnt[i] = 0;
-            O.aoff[i] = 0;
-            O.vol[i] = 0.f;
-            O.surf[i] = 0.f;
-            O.flags[i] = (uint8_t)(status == ST_OVERFLOW ? PD_CELL_OVERFLOW
-                                                         : (PD_CELL_EMPTY | (status == ST_DUP ? PD_CELL_DUPLICATE : 0)));
-        }
+        finalize_status(c, lane, P, status);
         return 0u;
     }
 #ifdef PD_SKIP_FIN
@@ -2032,7 +2146,7 @@ __global__ void __launch_bounds__(T::WARPS * 32) finalize_kernel(const __grid_co
             const auto t = (typename T::trip_t)rec[2 + np + u];
             double x, y, z;
             solve3(S.pl, ta(t), tb(t), tc(t), x, y, z);
-            put_vertex(S.fv, S.vx, S.vy, S.vz, u, x, y, z);
+            put_vertex(S, u, x, y, z);
             S.vt[u] = t;
         }
         __syncwarp();
@@ -2133,7 +2247,18 @@ __global__ void __launch_bounds__(T::WARPS * 32, T::MIN_BLOCKS) cells_kernel(con
             if (kStats<MODE> && st == ST_OVERFLOW) novf++;
             PT_BEGIN(t_fin);
             const bool deferred = kDefer<T> && st == ST_OK && P.rec_index && defer_cell(S, c, lane, P, s);
-            const unsigned rob = deferred ? 0u : finalize(S, c, lane, P, st);
+            unsigned rob = 0u;
+            if constexpr (T::F64V) {
+                if (!deferred) rob = finalize(S, c, lane, P, st);
+            } else {
+                // a finished cell whose record did not fit (never seen) is built again by the next tier; the
+                // cost-sampling runs (no records: only the work counts are read) skip the output
+                if (st == ST_OK && !deferred && P.rec_index) {
+                    if (lane == 0) P.next_list[atom_add_g32(P.next_count, 1)] = s;
+                    continue;
+                }
+                if (st != ST_OK) finalize_status(c, lane, P, st);
+            }
             if (rob && lane == 0) {  // robustness counters (rare, always published): straight to the device totals
                 red_add_g(&P.stats->dropped, rob & 0x7fffu);
                 red_add_g(&P.stats->small, (rob >> 15) & 0x7fffu);
@@ -2206,11 +2331,11 @@ cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num
         cudaError_t e = launch_tier1(p, st, num_sms);
         if (e != cudaSuccess || !p.rec_index) return e;
         if (launches) ++*launches;
-        const size_t smem = sizeof(WarpState<Tier1>) * Tier1::WARPS;
-        cudaFuncSetAttribute(finalize_kernel<Tier1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const size_t smem = sizeof(WarpState<Tier1F>) * Tier1F::WARPS;
+        cudaFuncSetAttribute(finalize_kernel<Tier1F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, finalize_kernel<Tier1>, Tier1::WARPS * 32, smem);
-        finalize_kernel<Tier1><<<num_sms * (per_sm < 1 ? 1 : per_sm), Tier1::WARPS * 32, smem, st>>>(p);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, finalize_kernel<Tier1F>, Tier1F::WARPS * 32, smem);
+        finalize_kernel<Tier1F><<<num_sms * (per_sm < 1 ? 1 : per_sm), Tier1::WARPS * 32, smem, st>>>(p);
         return cudaGetLastError();
     }
     if (tier == 1) return launch_tier<Tier2, kDynMode>(p, 1, st, num_sms);

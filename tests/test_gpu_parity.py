@@ -206,6 +206,21 @@ def test_top_tier_cooperative(cfg, n, flags, start_tier, monkeypatch):
     assert np.allclose(ref.volumes, g.volumes, rtol=1e-6)
 
 
+@pytest.mark.parametrize("cfg,n", [("C3", 8009), ("C4", 8009)])
+def test_record_arena_full(cfg, n, monkeypatch):
+    """Tier 1 keeps no FP64 vertices and always defers its finalize (a per-cell topology record that
+    finalize_kernel rebuilds); a finished cell whose record does not fit is built again by tier 2.  With a
+    tiny record arena (test knob PD_REC_CAP) most cells take that path: oracle parity, and the same
+    diagram as the default run."""
+    wl = pdgen.make(cfg, n=n)
+    ref = _gpu(wl)
+    monkeypatch.setenv("PD_REC_CAP", "20000")
+    g, o, rep = _assert_parity(wl, flags=pd.STATS)
+    assert g.stats["tier_cells"][1] > n // 2  # most cells really went to tier 2
+    assert np.array_equal(ref.offsets, g.offsets) and np.array_equal(ref.neighbors, g.neighbors)
+    assert np.allclose(ref.volumes, g.volumes, rtol=1e-6)
+
+
 @pytest.mark.parametrize("cfg,n", [("C1", None), ("C2", 4001), ("C3", 4001), ("C5", 4001)])
 def test_dual_tets_parity(cfg, n):
     """Dual tetrahedra (PD_TETS) equal the oracle's, as sets of sorted id
