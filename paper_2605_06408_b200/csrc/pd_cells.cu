@@ -46,8 +46,14 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PD_MATCH
 #define PD_MATCH 1
 #endif
+#ifndef PD_CLEAN_POP
+#define PD_CLEAN_POP 0  // tier 1: no re-validation at a pop when the cell has not changed since the last one (measured 10% slower on C4)
+#endif
 #ifndef PD_LAZY_COMPACT
 #define PD_LAZY_COMPACT 0  // swap-remove the popped queue entry while >= 3/4 are alive (all tiers)
+#endif
+#ifndef PD_LEAF_AABB
+#define PD_LEAF_AABB 0  // tier 1: the cell AABB refreshed once per leaf (after its clips), not after every clip
 #endif
 #ifndef PD_FUSED_AABB
 #define PD_FUSED_AABB 1  // tier 1: the new AABB from the classification pass (measured 3.5% faster on C4)
@@ -179,7 +185,7 @@ struct __align__(16) WarpState {
         struct {                  // traversal: priority queue of pushed child records
             float4 qlo[T::QMAX];  // (lo, maxw)
             float4 qhi[T::QMAX];  // (hi, link)
-            float qkey[PD_LAZY_POP ? T::QMAX : 1];  // priority at push time (lazy pop only)
+            float qkey[(PD_LAZY_POP || PD_CLEAN_POP) ? T::QMAX : 1];  // priority (lazy / clean pop)
         };
         struct {                  // finalize (the queue is dead by then)
             union {
@@ -303,6 +309,7 @@ enum { CLIP_NONE = 0, CLIP_DONE = 1, CLIP_EMPTY = 2, CLIP_OVF = 3 };
 struct Counters {
     unsigned long long nodes, leaves, sites, tests, clips, spills;
     unsigned work, visited;             // per cell
+    unsigned ncl;                       // clips so far (running; the traversal compares it across a leaf)
 #if PD_PROFILE
     unsigned long long cyc[10];  // init, descend, leaf, clip, pop, finalize | clip: classify, boundary, create, aabb
 #endif
@@ -356,6 +363,27 @@ __device__ __forceinline__ float dir_r2(const Cell& c, unsigned allow, bool iso)
 #ifndef PD_NODE_KEY
 #define PD_NODE_KEY 0  // default mode's queue priority: 0 Alg. 1's d^2 + min(0,dw) - r^2 (with bound (1)); 1 d^2 + min(0,dw)
 #endif
+// Priority (order only, the diagram is unchanged) with PK: a lower bound on the plane distance
+// d_ij = (|D|^2 + w_i - w_j) / (2|D|) of the node's sites (|D| >= d, w_j <= w_max).  As a function of
+// t = |D| it is minimal at t = sqrt(w_i - w_j) when w_i > w_j: the nearest planes of a heavy site come from
+// sites at distance ~sqrt(dw), not from the nearest boxes, so Alg. 1's distance order clips a heavy cell with
+// thousands of planes that later ones supersede.  Equal weights: d/2, the same order as d^2.
+#ifndef PD_PLANE_KEY
+#define PD_PLANE_KEY 2  // 0: Alg. 1's priority everywhere; 1: plane-distance bound in tiers 2-3; 2: in every tier
+#endif
+#ifndef PD_FAST_SQRT
+#define PD_FAST_SQRT 1  // bounds' square roots by MUFU.RSQ (no IEEE fix-up sequence), rounded up
+#endif
+// sqrt for the culling bounds (1e-5 relative margins): x * rsqrt(x) is within a few ulp; x (1 + 1e-6) covers it
+__device__ __forceinline__ float sqrt_up(float x) {
+    if (!PD_FAST_SQRT) return sqrtf(x);
+    return x > 0.f ? x * rsqrtf(x) * (1.f + 1e-6f) : 0.f;
+}
+__device__ __forceinline__ float plane_key(float d2, float dw) {
+    if (dw > 0.f && d2 < dw) return dw * rsqrtf(dw);  // sqrt(dw): approximate is fine, it only orders
+    return d2 > 0.f ? 0.5f * (d2 + dw) * rsqrtf(d2) : -INFINITY;
+}
+template <bool PK = false>
 __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi_l, unsigned flags, bool& culled) {
     const bool iso = (flags & PD_ISOTROPIC) != 0;
     const bool paper = (flags & (PD_PAPER_BOUND | PD_ISOTROPIC)) != 0;
@@ -380,7 +408,7 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
     float dw = c.fpw - lo_w.w;
     float dwn = fminf(0.f, dw);
     float r2 = dir_r2(c, allow, iso);
-    float rd = sqrtf(r2 * d2);
+    float rd = sqrt_up(r2 * d2);
     culled = d2 + dwn - 2.f * rd > 1e-5f * (d2 - dwn + 2.f * rd);
     if (!paper) {
         float h0 = fmaxf(fmaxf(c.flo[0] * a0, c.flo[0] * b0), fmaxf(c.fhi[0] * a0, c.fhi[0] * b0));
@@ -390,8 +418,13 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
         float mag = c.vmax * (fmaxf(fabsf(a0), fabsf(b0)) + fmaxf(fabsf(a1), fabsf(b1)) + fmaxf(fabsf(a2), fabsf(b2)));
         culled |= d2 + dw - 2.f * H > 1e-5f * (d2 + fabsf(dw) + 2.f * mag);
     }
+    if (PK) return plane_key(d2, dw);
     return d2 + dwn - r2;
 }
+template <class T>
+constexpr bool kCleanPop = PD_CLEAN_POP && !PD_LAZY_POP && !T::COOP;
+template <class T>
+constexpr bool kPlaneKey = PD_PLANE_KEY == 2 || (PD_PLANE_KEY == 1 && T::SPHERE);
 
 // ---------------------------------------------------------------- CTA-cooperative passes (top tier)
 // Warp 0 of a COOP CTA runs the cell program; at an O(V) pass it publishes a job in shared memory and
@@ -525,7 +558,7 @@ __device__ __forceinline__ void finish_aabb(Cell& c, const Box6& b) {
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 3; ++k) { c.flo[k] = lo[k]; c.fhi[k] = hi[k]; }
-    c.rmax = sqrtf(rm2);
+    c.rmax = sqrt_up(rm2);
     c.vmax = vm;
     __syncwarp();
 }
@@ -632,6 +665,13 @@ __device__ __forceinline__ void solve3(const double4* pl, int ia, int ib, int ic
     x *= inv; y *= inv; z *= inv;
 }
 
+#ifndef PD_SOLVE_OOL
+#define PD_SOLVE_OOL 0  // the new vertices' FP64 solve out of line (measured: not the register peak; kept off)
+#endif
+__device__ __noinline__ void solve3_ool(const double4* pl, int ia, int ib, int ic, double& x, double& y, double& z) {
+    solve3(pl, ia, ib, ic, x, y, z);
+}
+
 // FP64 position of vertex slot s: the stored copy, or (tiers without FP64 copies) re-solved from its plane
 // triplet exactly as it was created (solve3 on the same FP64 planes: the same value; box corners are exact).
 template <class T>
@@ -700,6 +740,9 @@ __device__ __forceinline__ bool outside_cert(const WarpState<T>& S, const Cell& 
 }
 
 template <class T>
+constexpr bool kLeafAabb = PD_LEAF_AABB && !T::COOP && !T::SPHERE;
+
+template <class T>
 __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, FPlane f, int pidn, Counters& cnt) {
     PT_BEGIN(t_cls);
     // warp-uniform counts snapshotted in registers; published to the shared Cell only at the end,
@@ -724,7 +767,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
             float s32 = fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d;
             if (fabsf(s32) > f.m) out = s32 > 0.f;
             else out = outside_cert(S, c, sj, f, s);
-            if (!out) box.add(v);
+            if (!kLeafAabb<T> && !out) box.add(v);
         }
         unsigned m = __ballot_sync(FULL, out);
         if (out) S.rem[R + __popc(m & lanemask_lt())] = (uint16_t)s;  // removed slots, ascending
@@ -855,11 +898,12 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
             uint32_t be = S.bnd[e];
             int x = be & 0xffff, y = be >> 16;
             double vx, vy, vz;
-            solve3(S.pl, hs, x, y, vx, vy, vz);
+            if (PD_SOLVE_OOL) solve3_ool(S.pl, hs, x, y, vx, vy, vz);
+            else solve3(S.pl, hs, x, y, vx, vy, vz);
             int slot = e < R ? S.rem[e] : nv0 + (e - R);
             put_vertex(S, slot, vx, vy, vz);
             S.vt[slot] = tpack<typename T::trip_t>(hs, x, y);
-            box.add(make_float4((float)vx, (float)vy, (float)vz, 0.f));
+            if (!kLeafAabb<T>) box.add(make_float4((float)vx, (float)vy, (float)vz, 0.f));
         }
     }
     // 4. if fewer vertices were created than removed, move kept vertices from the tail into holes
@@ -885,7 +929,9 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
     PT_BEGIN(t_ab);
     // fused: the AABB of the kept + created vertices gathered by this clip's passes (not in the
     // cooperative tier, whose classification runs on all warps, nor with the sphere bound)
-    if (PD_FUSED_AABB && !T::COOP && !T::SPHERE) finish_aabb(c, box);
+    // (a stale AABB contains the smaller cell: every bound that reads it stays sound, only looser)
+    if (kLeafAabb<T>) {
+    } else if (PD_FUSED_AABB && !T::COOP && !T::SPHERE) finish_aabb(c, box);
     else update_aabb(S, c, lane);
     PT_END(t_ab, 9);
     return CLIP_DONE;
@@ -1075,6 +1121,7 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         mask &= __reduce_or_sync(FULL, hit);
         cand = (mask >> lane) & 1u;
     }
+    int nclip = 0;
     while (mask) {
         int kmin = __reduce_min_sync(FULL, cand ? ford(key) : 0x7fffffff);
         unsigned lead = __ballot_sync(FULL, cand && ford(key) == kmin);
@@ -1114,7 +1161,9 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         if (st == CLIP_EMPTY) return ST_EMPTY;
         if (st == CLIP_OVF) return ST_OVERFLOW;
         if (st == CLIP_DONE) {
+            ++nclip;
             if (kStats<MODE>) cnt.clips++;
+            cnt.ncl++;
             cnt.work += 8;
             if (cand && site_culled_pl<T::SPHERE>(c, S.cpl[myslot], flags)) cand = false;
             if (PD_REFILTER && PD_PRETEST_COMPACT && !batched) {
@@ -1126,6 +1175,7 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         }
         mask = __ballot_sync(FULL, cand);
     }
+    if (kLeafAabb<T> && nclip) update_aabb(S, c, lane);
     return ST_OK;
 }
 
@@ -1183,6 +1233,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
     const int root_link = node;
     int ns = 0;  // spilled entries
     int nq = 0;  // queue length (warp-uniform register)
+    bool dirty = true;  // the cell changed since the queue was last re-validated (clean pop)
     for (;;) {
         if (have) {
             PT_BEGIN(t_desc);
@@ -1197,7 +1248,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 if (lane < WIDE) {
                     lo_w = __ldg(&rec[lane].lo_w);
                     hi_l = __ldg(&rec[lane].hi_l);
-                    if (__float_as_int(hi_l.w) != EMPTY_LINK) key = node_test(c, lo_w, hi_l, flags, culled);
+                    if (__float_as_int(hi_l.w) != EMPTY_LINK) key = node_test<kPlaneKey<T>>(c, lo_w, hi_l, flags, culled);
                 }
                 unsigned surv = __ballot_sync(FULL, !culled);
                 const bool ex_all = exact_on(flags, cnt.visited, P.exact_after);
@@ -1247,7 +1298,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     if (ns + tos > spill_cap) return ST_OVERFLOW;
                     if (push) {
                         if (rank < room) {
-                            if (PD_LAZY_POP) S.qkey[nq + rank] = key;
+                            if (PD_LAZY_POP || kCleanPop<T>) S.qkey[nq + rank] = key;
                             qlo[nq + rank] = lo_w;
                             qhi[nq + rank] = hi_l;
                         } else {
@@ -1266,9 +1317,11 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 if (kStats<MODE>) cnt.leaves++;
                 __syncwarp();
                 PT_BEGIN(t_leaf);
+                const unsigned ncl0 = cnt.ncl;
                 int st = process_leaf<T, MODE>(S, c, lane, node, warm, P, cnt);
                 PT_END(t_leaf, 2);
                 if (st != ST_OK) return st;
+                if (cnt.ncl != ncl0) dirty = true;
                 if (warm) {
                     warm = false;
                     node = root_link;
@@ -1281,12 +1334,13 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         __syncwarp();
         if (nq == 0 && ns > 0) {  // refill from the spill stack
             __threadfence_block();
+            dirty = true;  // refilled entries carry no key
             int mm = min(ns, T::QMAX);
             for (int t = lane; t < mm; t += 32) {
                 NodeChild e = spill[ns - mm + t];
                 if (PD_LAZY_POP) {
                     bool cu;
-                    S.qkey[t] = node_test(c, e.lo_w, e.hi_l, flags, cu);
+                    S.qkey[t] = node_test<kPlaneKey<T>>(c, e.lo_w, e.hi_l, flags, cu);
                 }
                 qlo[t] = e.lo_w;
                 qhi[t] = e.hi_l;
@@ -1301,7 +1355,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             while (nq > 0 && !ok) {
                 int t = nq - 1;
                 bool culled;
-                node_test(c, qlo[t], qhi[t], flags, culled);
+                node_test<kPlaneKey<T>>(c, qlo[t], qhi[t], flags, culled);
                 node = __float_as_int(qhi[t].w);
                 nq--;
                 ok = !culled;
@@ -1334,12 +1388,38 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             --nq;
             __syncwarp();
             bool culled;
-            node_test(c, lo, hi, flags, culled);
+            node_test<kPlaneKey<T>>(c, lo, hi, flags, culled);
             if (!culled && (exact_on(flags, cnt.visited, P.exact_after) ||
                             (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) && __float_as_int(hi.w) < 0)))
                 culled = node_exact_culled(S, c, lane, lo, hi);
             node = __float_as_int(hi.w);
             have = !culled;
+            PT_END(t_pop, 4);
+            continue;
+        }
+        if (kCleanPop<T> && !dirty && !dfs) {
+            // the cell is unchanged since the last re-validation: every queued entry is alive and its key
+            // current (entries pushed since were tested against this same cell); pop the least key
+            int bk = 0x7fffffff, bs = 0x7fffffff;
+            for (int sq = lane; sq < nq; sq += 32) {
+                const int k = ford(S.qkey[sq]);
+                if (k < bk) { bk = k; bs = sq; }
+            }
+            const int gk = __reduce_min_sync(FULL, bk);
+            const int bslot = __reduce_min_sync(FULL, bk == gk ? bs : 0x7fffffff);
+            node = __float_as_int(qhi[bslot].w);
+            const bool popped_dead = (exact_on(flags, cnt.visited, P.exact_after) ||
+                                      (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) && node < 0)) &&
+                                     node_exact_culled(S, c, lane, qlo[bslot], qhi[bslot]);
+            __syncwarp();
+            if (lane == 0 && bslot != nq - 1) {
+                qlo[bslot] = qlo[nq - 1];
+                qhi[bslot] = qhi[nq - 1];
+                S.qkey[bslot] = S.qkey[nq - 1];
+            }
+            __syncwarp();
+            --nq;
+            have = !popped_dead;
             PT_END(t_pop, 4);
             continue;
         }
@@ -1362,9 +1442,10 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             bool al = false;
             if (s < nq) {
                 bool culled;
-                float k = node_test(c, qlo[s], qhi[s], flags, culled);
+                float k = node_test<kPlaneKey<T>>(c, qlo[s], qhi[s], flags, culled);
                 al = !culled;
                 if (al && ford(k) < bestk) { bestk = ford(k); bests = s; }
+                if (kCleanPop<T>) S.qkey[s] = k;
             }
             unsigned am = __ballot_sync(FULL, al);
             if (lane == 0) qmask[ch] = am;
@@ -1407,18 +1488,24 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             bool keep = ((qmask[ch] >> lane) & 1u) && s != bslot;
             unsigned km = __ballot_sync(FULL, keep);
             float4 lo = make_float4(0, 0, 0, 0), hi = make_float4(0, 0, 0, 0);
-            if (keep) { lo = qlo[s]; hi = qhi[s]; }
+            float ky = 0.f;
+            if (keep) {
+                lo = qlo[s]; hi = qhi[s];
+                if (kCleanPop<T>) ky = S.qkey[s];
+            }
             __syncwarp();
             if (keep) {
                 int dst = base + __popc(km & lanemask_lt());
                 qlo[dst] = lo;
                 qhi[dst] = hi;
+                if (kCleanPop<T>) S.qkey[dst] = ky;
             }
             __syncwarp();
             base += __popc(km);
         }
         nq = base;
         have = !popped_dead;
+        dirty = false;
         PT_END(t_pop, 4);
     }
 }
@@ -1468,7 +1555,7 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 3; ++k) { c.flo[k] = flo[k]; c.fhi[k] = fhi[k]; }
-    c.rmax = sqrtf(rm2);
+    c.rmax = sqrt_up(rm2);
     c.vmax = vm;
     __syncwarp();
 }
@@ -1869,7 +1956,7 @@ __device__ __forceinline__ void coop_run(WarpState<T>& S, CoopJob& J, int w, int
             bool al = false;
             if (sq < nq) {
                 bool culled;
-                const float k = node_test(c, qlo[sq], qhi[sq], flags, culled);
+                const float k = node_test<kPlaneKey<T>>(c, qlo[sq], qhi[sq], flags, culled);
                 al = !culled;
                 if (al && ford(k) < bestk) { bestk = ford(k); bests = sq; }
             }
