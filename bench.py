@@ -312,11 +312,13 @@ def run_ours(args):
         roof = {"bound": "alu", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak,
                 "traffic": met.get("dram_bytes_per_launch") if met else None,
-                "kernel": "cells_kernel (3 capacity tiers, one launch each)",
+                "kernel": "cells_kernel (3 capacity tiers, one launch each) + the tier-1 finalize_kernel",
                 "kernel_ms": kms, "kernel_share_of_step": kms / ms if world == 1 else None,
                 "work_model": "achieved = W_min 2.3e4 FP32 lane-ops/cell (SURVEY.md §8(d)) x cells of this rank / "
-                              "cell-kernel time (CUDA events on the launching stream); peak = FFMA-chain "
-                              "microbenchmark on this GPU in this job (pd_measure_fp32_peak)",
+                              "cell-kernel time (CUDA events on the launching stream around the tier launches "
+                              "and the finalize); peak = FFMA-chain microbenchmark on this GPU in this job "
+                              "(pd_measure_fp32_peak); traffic and ncu_* = the tier-1 cells_kernel launch "
+                              "(ncu_source)",
                 "fp32_peak_measured": fp32_peak, "fp32_peak_nominal": ALU_PEAK_TOPS,
                 "l2_peak_measured": l2_peak, "frac_useful": achieved / fp32_peak}
         if met:  # what the counters say (ncu capture of the same code, profiles/)

@@ -73,14 +73,19 @@ enum {
                                     all, the pre-clip only where it pays (heavy-tailed weights) */
     PD_TETS = 1u << 11,       /* also output the dual tetrahedra (the "explicit mesh"
                                  of PAPER.md:343/398): see pd_tets.  Not with shard_world > 1 (PD_EINVAL). */
-    PD_NO_AUTO_WARM = 1u << 13 /* never switch the KNN warm start on by itself.  Default: with weights and neither
-                                  PD_WARM_START nor PD_WARM_ADAPTIVE given, the tier-1 cell program runs on a strided
-                                  8k-site sample with and without the KNN pre-clip (deterministic per-cell work
-                                  counters, PD_COST) and PD_WARM_START is used when sampled work with it (x 1.10, plus
-                                  ~60 units per site for the KNN query) is below 0.9 x the work without
-                                  (pd_stats.warm_gain).  Costs two sample launches + one sync (~5 ms); every rank of
-                                  a sharded build measures the same sample and takes the same decision.  The diagram
-                                  is the same either way (areas/volumes to rounding). */
+    PD_NO_AUTO_WARM = 1u << 13, /* accepted for compatibility: the automatic warm-start decision is now opt-in
+                                   (PD_AUTO_WARM), so this is the default */
+    PD_AUTO_WARM = 1u << 14   /* decide the KNN warm start by measurement: with weights and neither PD_WARM_START
+                                  nor PD_WARM_ADAPTIVE given, the tier-1 cell program runs on a strided 8k-site
+                                  sample with and without the KNN pre-clip (deterministic per-cell work counters,
+                                  PD_COST) and PD_WARM_START is used when sampled work with it (x 1.10, plus ~60
+                                  units per site for the KNN query) is below 0.9 x the work without
+                                  (pd_stats.warm_gain).  Costs two sample launches + one sync (~2-5 ms); every rank
+                                  of a sharded build measures the same sample and takes the same decision.  Off by
+                                  default since the queue priority became the plane-distance bound:
+                                  the warm start then measured slower on every configuration (C3 170 -> 280 ms,
+                                  C4 381 -> 636 ms, C5 632 -> 1079 ms) and the sample alone cost ~0.5% of C4.  The
+                                  diagram is the same either way (areas/volumes to rounding). */
 };
 
 /* pd_cell_flags values */

@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(HERE, "libpd.so")
 PD_OK, PD_EINVAL, PD_EEMPTY, PD_ENONFINITE, PD_EOUTSIDE, PD_ENOMEM, PD_ECUDA, PD_ENCCL, PD_EINTERNAL = range(9)
 IN_DEVICE, OUT_HOST, STATS, ISOTROPIC, DFS, PAPER_BOUND, COST, EXACT_NODES, NO_EXACT, BALANCE = (
     1, 2, 4, 8, 16, 64, 128, 256, 512, 1024)
-WARM_START, TETS, WARM_ADAPTIVE, NO_AUTO_WARM = 32, 2048, 4096, 8192
+WARM_START, TETS, WARM_ADAPTIVE, NO_AUTO_WARM, AUTO_WARM = 32, 2048, 4096, 8192, 16384
 CELL_EMPTY, CELL_BOUNDARY, CELL_OVERFLOW, CELL_DUPLICATE, CELL_DEGRADED, CELL_NOT_OWNED = 1, 2, 4, 8, 16, 32
 
 EXPORTED = ["pd_build", "pd_num_cells", "pd_nnz", "pd_on_host", "pd_offsets", "pd_neighbors", "pd_face_areas",

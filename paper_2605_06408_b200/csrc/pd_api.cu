@@ -514,11 +514,12 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             ck(cudaStreamSynchronize(st));  // hpos is a host temporary
             return spos;
         };
-        // ---- auto warm start (pd.h PD_NO_AUTO_WARM): measure the sampled tier-1 work with and without the KNN
+        // ---- auto warm start (pd.h PD_AUTO_WARM): measure the sampled tier-1 work with and without the KNN
         // pre-clip and keep it when it saves more than the KNN query costs
         double warm_gain = 0.0;
         int32_t* knn = nullptr;
-        if (!(opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE | PD_NO_AUTO_WARM)) && n >= 4096 && (weights || comm)) {
+        if ((opt.flags & PD_AUTO_WARM) && !(opt.flags & (PD_WARM_START | PD_WARM_ADAPTIVE | PD_NO_AUTO_WARM)) &&
+            n >= 4096 && (weights || comm)) {
             int64_t ns = 0, stride = 1;
             const int32_t* spos = strided_sample(8192, ns, stride);
             int32_t* scount = W.alloc<int32_t>(4);

@@ -89,8 +89,11 @@ constexpr unsigned FULL = 0xffffffffu;
 #define PD_PRETEST_COMPACT 1  // the pre-test's candidate planes packed by rank (no empty groups of 4)
 #endif
 
-template <int V, int P, int Q, int W, int MINB, bool GLOB = false, bool CO = false, bool SPH = false, bool F64 = true>
+template <int V, int P, int Q, int W, int MINB, bool GLOB = false, bool CO = false, bool SPH = false, bool F64 = true,
+          bool FINAL = false>
 struct TierCfg {
+    // the state of finalize_kernel only: no clipping scratch (candidate planes, plane-GC map)
+    static constexpr bool FIN = FINAL;
     // FP64 vertex copies in the state.  Tier 1 keeps none (its finalize is deferred to finalize_kernel, which
     // rebuilds every vertex from its plane triplet): the rare FP64 certification of an ambiguous FP32
     // classification re-solves the vertex from its three FP64 planes instead (same solve3, same operands).
@@ -136,7 +139,7 @@ struct TierCfg {
 #endif
 using Tier1 = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, PD_T1_WARPS, PD_T1_MINB, false, false, PD_T1_SPHERE != 0, PD_T1_F64V != 0>;
 // the state finalize_kernel rebuilds a deferred tier-1 cell into (with the FP64 vertices finalize() reads)
-using Tier1F = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, PD_T1_WARPS, PD_T1_MINB, false, false, PD_T1_SPHERE != 0, true>;
+using Tier1F = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, PD_T1_WARPS, PD_T1_MINB, false, false, PD_T1_SPHERE != 0, true, true>;
 // Tier 2: one cell per CTA of 4 warps (state in shared memory, O(V) passes CTA-wide from 128 vertices):
 // the few heavy cells of a light-weight workload (C4: 78) no longer run on one warp each, which
 // mattered most for the per-rank critical path of sharded builds.
@@ -214,9 +217,9 @@ struct __align__(16) WarpState {
     uint32_t omask[T::VC];        // outside-vertex ballots of the current clip
     uint32_t qmask[T::QC];        // alive-entry ballots of the current pop
     uint32_t bnd[T::VMAX];        // boundary edges (x | y << 16) of the current clip (B <= VMAX unless overflow)
-    uint16_t pmap[T::PMAX];       // plane GC remap
-    float4 cpl[32];               // a leaf's candidates, lane = candidate: FP32 plane (D = p_j - p_i, dd = q/2)
-    __align__(16) float cmg[32];  //   and its certification margin (kept in smem, not registers, through clip())
+    uint16_t pmap[T::FIN ? 1 : T::PMAX];  // plane GC remap
+    float4 cpl[T::FIN ? 1 : 32];  // a leaf's candidates, by rank: FP32 plane (D = p_j - p_i, dd = q/2)
+    __align__(16) float cmg[T::FIN ? 4 : 32];  //   and its certification margin (kept in smem, not registers, through clip())
     uint32_t ebits[T::EBW];       // hole-edge parity bitmap (zero between clips)
 };
 
@@ -372,7 +375,7 @@ __device__ __forceinline__ float dir_r2(const Cell& c, unsigned allow, bool iso)
 #define PD_PLANE_KEY 2  // 0: Alg. 1's priority everywhere; 1: plane-distance bound in tiers 2-3; 2: in every tier
 #endif
 #ifndef PD_FAST_SQRT
-#define PD_FAST_SQRT 1  // bounds' square roots by MUFU.RSQ (no IEEE fix-up sequence), rounded up
+#define PD_FAST_SQRT 0  // bounds' square roots by MUFU.RSQ, rounded up (measured no different on C2-C5; IEEE sqrtf kept)
 #endif
 // sqrt for the culling bounds (1e-5 relative margins): x * rsqrt(x) is within a few ulp; x (1 + 1e-6) covers it
 __device__ __forceinline__ float sqrt_up(float x) {
@@ -418,13 +421,14 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
         float mag = c.vmax * (fmaxf(fabsf(a0), fabsf(b0)) + fmaxf(fabsf(a1), fabsf(b1)) + fmaxf(fabsf(a2), fabsf(b2)));
         culled |= d2 + dw - 2.f * H > 1e-5f * (d2 + fabsf(dw) + 2.f * mag);
     }
+    if (PK && PD_PLANE_KEY == 3) return plane_key(d2, dw) - sqrtf(r2);  // the nearest plane's depth in the cell
     if (PK) return plane_key(d2, dw);
     return d2 + dwn - r2;
 }
 template <class T>
 constexpr bool kCleanPop = PD_CLEAN_POP && !PD_LAZY_POP && !T::COOP;
 template <class T>
-constexpr bool kPlaneKey = PD_PLANE_KEY == 2 || (PD_PLANE_KEY == 1 && T::SPHERE);
+constexpr bool kPlaneKey = PD_PLANE_KEY >= 2 || (PD_PLANE_KEY == 1 && T::SPHERE);
 
 // ---------------------------------------------------------------- CTA-cooperative passes (top tier)
 // Warp 0 of a COOP CTA runs the cell program; at an O(V) pass it publishes a job in shared memory and

@@ -163,6 +163,18 @@ def test_warm_start_parity(cfg, n):
     _assert_parity(pdgen.make(cfg, n=n), flags=pd.WARM_ADAPTIVE)
 
 
+@pytest.mark.parametrize("cfg,n", [("C3", 20011), ("C5", 20011)])
+def test_auto_warm_decision(cfg, n):
+    """PD_AUTO_WARM: the sampled warm-start decision runs (warm_gain > 0 reported), the diagram matches the
+    oracle and the default build's neighbour sets whichever way it decides."""
+    wl = pdgen.make(cfg, n=n)
+    ref = _gpu(wl)
+    g, o, rep = _assert_parity(wl, flags=pd.AUTO_WARM)
+    assert g.stats["warm_gain"] > 0 and g.stats["warm_start"] in (0, 1)
+    assert np.array_equal(ref.offsets, g.offsets) and np.array_equal(ref.neighbors, g.neighbors)
+    assert _gpu(wl).stats["warm_gain"] == 0  # default: no sampling
+
+
 def test_warm_start_duplicates_and_lattice():
     """Warm start with coincident sites (excluded from the KNN; the leaf processing decides ownership)
     and with cospherical lattices (KNN planes met again in their leaves must not re-clip)."""

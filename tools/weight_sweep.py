@@ -2,8 +2,8 @@
 its real "bicycle" scene, 0.595 s -> 2.243 s as the empty ratio goes 0 -> 0.468).  Here: the scene-like C4 positions
 (10M) with the paper's weight law scaled by s, w ~ N(0, (s d_nn^2/3)^2) (the
 paper's "weight ratio" unit is not recoverable from its text, SURVEY.md §8(c) Q13 / DESIGN.md R16), so s is swept
-until the empty ratio passes the paper's 0.47.  Each s is timed with the default options (auto warm start) and with
-PD_NO_AUTO_WARM; time = pd_build end to end (ms_total, CUDA events in the library), median of 5 after 3 warm-ups.
+until the empty ratio passes the paper's 0.47.  Each s is timed with the default options and with PD_AUTO_WARM
+(the sampled warm-start decision); time = pd_build end to end (ms_total, CUDA events in the library), median of 5 after 3 warm-ups.
 
     python tools/weight_sweep.py [n=10000000]  -> one JSON line per (s, mode)
 """
@@ -29,7 +29,7 @@ def main():
     for s in [0.0, 1.0, 3.0, 10.0, 30.0, 100.0, 300.0, 1000.0]:
         w = pdgen.weights_paper(n, d_nn, 4, ratio=s) if s > 0 else None
         wt = None if w is None else torch.from_numpy(w).cuda()
-        for mode, flags in (("default", 0), ("no_auto_warm", pd.NO_AUTO_WARM)):
+        for mode, flags in (("default", 0), ("auto_warm", pd.AUTO_WARM)):
             ms = []
             for it in range(8):
                 d = pd.build_diagram(pt, wt, pdgen.OMEGA_BOX, flags=flags)
