@@ -26,6 +26,7 @@
 //   * capacity tiers: cells that outgrow the tier's on-chip arrays are handed to a larger tier.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <assert.h>
 #include <stdio.h>
 
 #include <type_traits>
@@ -36,6 +37,13 @@ namespace pd {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+// Bounds checks of the on-chip arrays (a -DPD_CHECKS build: device asserts; tools/checks.sh runs the GPU parity
+// tests under it).  Compiled out of the product build.
+#ifdef PD_CHECKS
+#define PD_ASSERT(c) assert(c)
+#else
+#define PD_ASSERT(c) (void)0
+#endif
 
 #ifndef PD_LAZY_POP
 #define PD_LAZY_POP 0
@@ -404,7 +412,7 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
         const float H = h0 + h1 + h2;
         const float mag = c.vmax * (fmaxf(fabsf(a0), fabsf(b0)) + fmaxf(fabsf(a1), fabsf(b1)) + fmaxf(fabsf(a2), fabsf(b2)));
         culled = d2 + dw - 2.f * H > 1e-5f * (d2 + fabsf(dw) + 2.f * mag);
-        return d2 + fminf(0.f, dw);
+        return PK ? plane_key(d2, dw) : d2 + fminf(0.f, dw);
     }
     unsigned allow = (b0 >= 0.f ? 1u : 0u) | (a0 <= 0.f ? 2u : 0u) | (b1 >= 0.f ? 4u : 0u) | (a1 <= 0.f ? 8u : 0u) |
                      (b2 >= 0.f ? 16u : 0u) | (a2 <= 0.f ? 32u : 0u);
@@ -774,7 +782,10 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
             if (!kLeafAabb<T> && !out) box.add(v);
         }
         unsigned m = __ballot_sync(FULL, out);
-        if (out) S.rem[R + __popc(m & lanemask_lt())] = (uint16_t)s;  // removed slots, ascending
+        if (out) {
+            PD_ASSERT(R + __popc(m & lanemask_lt()) < T::VMAX);
+            S.rem[R + __popc(m & lanemask_lt())] = (uint16_t)s;  // removed slots, ascending
+        }
         if (lane == 0) S.omask[ch] = m;
         R += __popc(m);
     }
@@ -892,6 +903,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
     // 3. append the plane, create (h, x, y) for every boundary edge
     int hs = np0;
     if (lane == 0) {  // the exact FP64 plane goes straight to shared memory (read back by every new vertex)
+        PD_ASSERT(hs < T::PMAX);
         S.pl[hs] = exact_plane(c, sj);
         S.pid[hs] = pidn;
     }
@@ -906,6 +918,7 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
             else solve3(S.pl, hs, x, y, vx, vy, vz);
             int slot = e < R ? S.rem[e] : nv0 + (e - R);
             put_vertex(S, slot, vx, vy, vz);
+            PD_ASSERT(slot >= 0 && slot < T::VMAX && x < hs && y < hs && x != y);
             S.vt[slot] = tpack<typename T::trip_t>(hs, x, y);
             if (!kLeafAabb<T>) box.add(make_float4((float)vx, (float)vy, (float)vz, 0.f));
         }
@@ -1303,6 +1316,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     if (push) {
                         if (rank < room) {
                             if (PD_LAZY_POP || kCleanPop<T>) S.qkey[nq + rank] = key;
+                            PD_ASSERT(nq + rank < T::QMAX);
                             qlo[nq + rank] = lo_w;
                             qhi[nq + rank] = hi_l;
                         } else {
@@ -2204,6 +2218,7 @@ __global__ void __launch_bounds__(T::WARPS * 32) finalize_kernel(const __grid_co
         const uint32_t* rec = P.rec_arena + off;
         const uint32_t h0 = rec[0];
         const int nv = (int)(h0 & 0xffffu), np = (int)(h0 >> 16);
+        PD_ASSERT(nv >= 4 && nv <= T::VMAX && np >= 4 && np <= T::PMAX && off + 2u + (uint32_t)(nv + np) <= P.rec_cap);
         const float4 site = __ldg(&P.sites[s]);
         __syncwarp();
         if (lane == 0) {

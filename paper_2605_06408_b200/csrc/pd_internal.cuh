@@ -98,7 +98,7 @@ struct CellParams {
     uint32_t* rec_index;           // per Morton position: word offset of its record, ~0u = not deferred
     uint32_t* rec_arena;           // records: [nv | np << 16, degraded, pid[np], vt[nv]]
     unsigned long long* rec_top;   // bump pointer (words)
-    int64_t rec_cap;               // words (< 2^32); a cell that does not fit is finalized in the cell kernel
+    int64_t rec_cap;               // words (< 2^32); a cell that does not fit is built again by tier 2
 };
 
 cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches);

@@ -23,4 +23,5 @@ run synccheck_c5_tier3 synccheck PD_START_TIER=2 PD_COOP_MIN_V=0 $CS --tool sync
 run synccheck_c1 synccheck $CS --tool synccheck $PY C1 0
 run initcheck_c1 initcheck $CS --tool initcheck $PY C1 0
 run initcheck_c5_20k initcheck $CS --tool initcheck $PY C5 20000
+run memcheck_recfull memcheck PD_REC_CAP=20000 $CS --tool memcheck $PY C4 8000 0
 tail -n 4 gpurun_out/san_*.log
