@@ -449,8 +449,8 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
         pd::NodeChild* spill = W.alloc<pd::NodeChild>(spill_entries);
         void* gstate = W.alloc<unsigned char>(pd::cells_global_state_bytes(sms));
         const int exact_after = [] {
-            const char* ev = getenv("PD_EXACT_AFTER");  // tuning knob (default 200)
-            return ev ? atoi(ev) : 200;
+            const char* ev = getenv("PD_EXACT_AFTER");  // tuning knob (default 100: C3 -2% vs 200, C4 unchanged)
+            return ev ? atoi(ev) : 100;
         }();
         // ---- slice of the Morton order owned by this rank: equal-count by default;
         // PD_BALANCE cuts equal estimated cost, from the tier-1 kernel's per-cell work counters on a

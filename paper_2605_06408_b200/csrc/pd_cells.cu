@@ -87,6 +87,15 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PD_PRETEST
 #define PD_PRETEST 1  // per leaf: every candidate against every vertex at once (lane = vertex), FP32 only
 #endif
+#ifndef PD_INL_EXACT
+#define PD_INL_EXACT __noinline__  // the exact polytope-vs-box node test (rare unless PD_EXACT_LEAVES)
+#endif
+#ifndef PD_FLAT_NODES
+#define PD_FLAT_NODES 1  // descent: node tests on all 32 lanes (child lane & 7) instead of a lane < 8 branch
+#endif
+#ifndef PD_FLAT_CLASSIFY
+#define PD_FLAT_CLASSIFY 1  // clip classification without divergent branches (certification behind a warp vote)
+#endif
 #ifndef PD_REFILTER
 #define PD_REFILTER 0  // re-run the pre-test on a leaf's remaining candidates after each clip
 #endif
@@ -518,7 +527,7 @@ __device__ __forceinline__ void coop_go(WarpState<T>& S, CoopJob& J, int lane) {
 }
 
 template <class T>
-__device__ __noinline__ bool node_exact_culled(const WarpState<T>& S, const Cell& c, int lane, float4 lo_w, float4 hi_l) {
+__device__ PD_INL_EXACT bool node_exact_culled(const WarpState<T>& S, const Cell& c, int lane, float4 lo_w, float4 hi_l) {
     float best;
     if (T::COOP && c.nv >= P_coop_min_v(S)) {
         CoopJob& J = coop_job();
@@ -774,6 +783,18 @@ __device__ PD_INL_CLIP int clip(WarpState<T>& S, Cell& c, int lane, float4 sj, F
     for (int ch = 0; ch < nch; ++ch) {
         int s = ch * 32 + lane;
         bool out = false;
+        if (PD_FLAT_CLASSIFY) {
+            // branch-free: every lane loads a valid slot and the rare FP64 certification is a warp-uniform branch
+            const bool in = s < nv0;
+            const float4 v = S.fv[in ? s : 0];
+            const float s32 = fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d;
+            out = in && s32 > f.m;
+            const bool amb = in && fabsf(s32) <= f.m;
+            if (__any_sync(FULL, amb)) {
+                if (amb) out = outside_cert(S, c, sj, f, s);
+            }
+            if (!kLeafAabb<T> && in && !out) box.add(v);
+        } else
         if (s < nv0) {
             float4 v = S.fv[s];
             float s32 = fmaf(f.nx, v.x, fmaf(f.ny, v.y, f.nz * v.z)) - f.d;
@@ -1262,7 +1283,12 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 bool culled = true;
                 float4 lo_w = make_float4(0, 0, 0, 0), hi_l = make_float4(0, 0, 0, 0);
                 const NodeChild* rec = P.nodes[node].c;
-                if (lane < WIDE) {
+                if (PD_FLAT_NODES) {  // every lane tests child lane & 7 (no divergent branch); lanes >= 8 are culled
+                    lo_w = __ldg(&rec[lane & (WIDE - 1)].lo_w);
+                    hi_l = __ldg(&rec[lane & (WIDE - 1)].hi_l);
+                    key = node_test<kPlaneKey<T>>(c, lo_w, hi_l, flags, culled);
+                    culled = culled || lane >= WIDE || __float_as_int(hi_l.w) == EMPTY_LINK;
+                } else if (lane < WIDE) {
                     lo_w = __ldg(&rec[lane].lo_w);
                     hi_l = __ldg(&rec[lane].hi_l);
                     if (__float_as_int(hi_l.w) != EMPTY_LINK) key = node_test<kPlaneKey<T>>(c, lo_w, hi_l, flags, culled);
@@ -1272,7 +1298,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 // exact test on every surviving LEAF child (a leaf costs far more than the test), and on
                 // internal children too once the cell is heavy
                 const unsigned leafm = __ballot_sync(FULL, lane < WIDE && __float_as_int(hi_l.w) < 0);
-                const unsigned exm = ex_all ? surv : (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) ? (surv & leafm) : 0u);
+                const unsigned exm = ex_all ? surv : (PD_EXACT_LEAVES == 1 && !(flags & PD_NO_EXACT) ? (surv & leafm) : 0u);
                 if (exm && T::COOP && c.nv >= P_coop_min_v(S)) {  // all children in one CTA-wide pass
                     CoopJob& J = coop_job();
                     const bool mine = lane < WIDE && ((exm >> lane) & 1u);
@@ -1327,6 +1353,14 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     nq += npush - tos;
                     ns += tos;
                     if (kStats<MODE>) cnt.spills += tos;
+                }
+                // PD_EXACT_LEAVES 2: the leaf about to be processed gets the exact polytope-vs-box test (a leaf
+                // costs far more than one warp pass over the vertices; 60% of the leaves the AABB tests keep fail it)
+                if (PD_EXACT_LEAVES == 2 && lnear < 0 && !ex_all && !(flags & PD_NO_EXACT) &&
+                    node_exact_culled(S, c, lane, __ldg(&rec[near].lo_w), __ldg(&rec[near].hi_l))) {
+                    have = false;
+                    PT_END(t_desc, 1);
+                    break;
                 }
                 node = lnear;
             }
@@ -1458,6 +1492,14 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         for (int ch = 0; ch < qch; ++ch) {
             int s = ch * 32 + lane;
             bool al = false;
+            if (PD_FLAT_NODES) {  // no divergent branch: lanes past the queue test slot 0 and are dropped
+                const bool in = s < nq;
+                bool culled;
+                const float k = node_test<kPlaneKey<T>>(c, qlo[in ? s : 0], qhi[in ? s : 0], flags, culled);
+                al = in && !culled;
+                if (al && ford(k) < bestk) { bestk = ford(k); bests = s; }
+                if (kCleanPop<T> && in) S.qkey[s] = k;
+            } else
             if (s < nq) {
                 bool culled;
                 float k = node_test<kPlaneKey<T>>(c, qlo[s], qhi[s], flags, culled);
