@@ -185,7 +185,6 @@ struct Cell {
     float fpx, fpy, fpz, fpw;
     float flo[3], fhi[3];   // cell AABB, site-local, rounded outward
     float vmax;             // max_k max(|lo_k|, |hi_k|)
-    float rmax;             // max corner distance of the AABB (isotropic radius bound)
     float sc[3], srad;      // bounding sphere of the cell (SPHERE tiers): center (site-local), radius
     int nv, np, nq;
     int degraded;           // a topology-consistency check failed (PD_CELL_DEGRADED)
@@ -350,6 +349,23 @@ struct FPlane {
     float nx, ny, nz, d, m;
 };
 // FP64 certification tolerance 1e-12 |n| R (reading R9), in FP32; only evaluated on the rare certification path.
+#ifndef PD_FAST_SQRT
+#define PD_FAST_SQRT 0  // bounds' square roots by MUFU.RSQ, rounded up (measured no different on C2-C5; IEEE sqrtf kept)
+#endif
+// sqrt for the culling bounds (1e-5 relative margins): x * rsqrt(x) is within a few ulp; x (1 + 1e-6) covers it
+__device__ __forceinline__ float sqrt_up(float x) {
+    if (!PD_FAST_SQRT) return sqrtf(x);
+    return x > 0.f ? x * rsqrtf(x) * (1.f + 1e-6f) : 0.f;
+}
+// Max corner distance of the cell AABB (the isotropic radius R of P:211 and the scale of the FP64 certification
+// tolerance, R9): computed where it is used (rarely: certification, isotropic ablation) from the stored AABB.
+__device__ __forceinline__ float cell_r2(const Cell& c) {
+    float rm2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) rm2 += fmaxf(c.flo[k] * c.flo[k], c.fhi[k] * c.fhi[k]);
+    return rm2;
+}
+__device__ __forceinline__ float cell_rmax(const Cell& c) { return sqrt_up(cell_r2(c)); }
 __device__ __forceinline__ float cert_tol(const FPlane& f, float rmax) {
     const float f2 = f.nx * f.nx + f.ny * f.ny + f.nz * f.nz;
     return 1e-12f * (f2 * rsqrtf(f2)) * rmax;
@@ -391,14 +407,6 @@ __device__ __forceinline__ float dir_r2(const Cell& c, unsigned allow, bool iso)
 #ifndef PD_PLANE_KEY
 #define PD_PLANE_KEY 2  // 0: Alg. 1's priority everywhere; 1: plane-distance bound in tiers 2-3; 2: in every tier
 #endif
-#ifndef PD_FAST_SQRT
-#define PD_FAST_SQRT 0  // bounds' square roots by MUFU.RSQ, rounded up (measured no different on C2-C5; IEEE sqrtf kept)
-#endif
-// sqrt for the culling bounds (1e-5 relative margins): x * rsqrt(x) is within a few ulp; x (1 + 1e-6) covers it
-__device__ __forceinline__ float sqrt_up(float x) {
-    if (!PD_FAST_SQRT) return sqrtf(x);
-    return x > 0.f ? x * rsqrtf(x) * (1.f + 1e-6f) : 0.f;
-}
 __device__ __forceinline__ float plane_key(float d2, float dw) {
     if (dw > 0.f && d2 < dw) return dw * rsqrtf(dw);  // sqrt(dw): approximate is fine, it only orders
     return d2 > 0.f ? 0.5f * (d2 + dw) * rsqrtf(d2) : -INFINITY;
@@ -565,13 +573,12 @@ __device__ __forceinline__ void finish_aabb(Cell& c, const Box6& b) {
     hi[0] = iford(__reduce_max_sync(FULL, ford(b.hi0)));
     hi[1] = iford(__reduce_max_sync(FULL, ford(b.hi1)));
     hi[2] = iford(__reduce_max_sync(FULL, ford(b.hi2)));
-    float rm2 = 0.f, vm = 0.f;
+    float vm = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         // the FP32 copies are rounded to nearest: widen by 2 ulp so the box contains the FP64 cell
         lo[k] -= fabsf(lo[k]) * 2.4e-7f + 1e-30f;
         hi[k] += fabsf(hi[k]) * 2.4e-7f + 1e-30f;
-        rm2 += fmaxf(lo[k] * lo[k], hi[k] * hi[k]);
         vm = fmaxf(vm, fmaxf(-lo[k], hi[k]));
     }
     // every lane writes the same warp-uniform fields: no lane may still be reading the old ones, and all
@@ -579,7 +586,6 @@ __device__ __forceinline__ void finish_aabb(Cell& c, const Box6& b) {
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 3; ++k) { c.flo[k] = lo[k]; c.fhi[k] = hi[k]; }
-    c.rmax = sqrt_up(rm2);
     c.vmax = vm;
     __syncwarp();
 }
@@ -743,7 +749,7 @@ __device__ __noinline__ int rem_from_omask(WarpState<T>& S, int nch, int lane) {
 // hot loop carries no FP64 set-up.
 __device__ __forceinline__ bool outside_fp64(const Cell& c, float4 sj, const FPlane& f, double vx, double vy, double vz) {
     const double4 pe = exact_plane(c, sj);
-    return fma(pe.x, vx, fma(pe.y, vy, pe.z * vz)) - pe.w > (double)cert_tol(f, c.rmax);
+    return fma(pe.x, vx, fma(pe.y, vy, pe.z * vz)) - pe.w > (double)cert_tol(f, cell_rmax(c));
 }
 
 // The FP64 certification of an ambiguous FP32 classification (rare).  Out of line in the tiers without FP64
@@ -997,7 +1003,7 @@ __device__ __forceinline__ bool site_culled_hq(const Cell& c, float Dx, float Dy
     }
     float r2;
     if (flags & PD_ISOTROPIC) {
-        r2 = c.rmax * c.rmax;
+        r2 = cell_r2(c);
     } else {
         float hx = Dx >= 0.f ? c.fhi[0] : c.flo[0], hy = Dy >= 0.f ? c.fhi[1] : c.flo[1], hz = Dz >= 0.f ? c.fhi[2] : c.flo[2];
         r2 = hx * hx + hy * hy + hz * hz;
@@ -1022,7 +1028,7 @@ template <class T>
 __device__ __noinline__ bool cuts_fp64(const WarpState<T>& S, const Cell& c, float4 sj, float D2) {
     double ex = (double)sj.x - c.px, ey = (double)sj.y - c.py, ez = (double)sj.z - c.pz;
     double ed = 0.5 * (ex * ex + ey * ey + ez * ez + (c.pw - (double)sj.w));
-    double tol = 1e-12 * (double)sqrtf(D2) * (double)c.rmax;
+    double tol = 1e-12 * (double)sqrtf(D2) * (double)cell_rmax(c);
     for (int k = 0; k < c.nv; ++k) {
         double x, y, z;
         vertex64(S, k, x, y, z);
@@ -1602,20 +1608,18 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
     }
     // the AABB of the box's corners: what update_aabb computes from their FP32 copies, without the warp reductions
     // (keeps the once-per-cell code small: it shares the instruction cache with the hot loop)
-    float rm2 = 0.f, vm = 0.f, flo[3], fhi[3];
+    float vm = 0.f, flo[3], fhi[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         flo[k] = (float)lo[k];
         fhi[k] = (float)hi[k];
         flo[k] -= fabsf(flo[k]) * 2.4e-7f + 1e-30f;
         fhi[k] += fabsf(fhi[k]) * 2.4e-7f + 1e-30f;
-        rm2 += fmaxf(flo[k] * flo[k], fhi[k] * fhi[k]);
         vm = fmaxf(vm, fmaxf(-flo[k], fhi[k]));
     }
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 3; ++k) { c.flo[k] = flo[k]; c.fhi[k] = fhi[k]; }
-    c.rmax = sqrt_up(rm2);
     c.vmax = vm;
     __syncwarp();
 }
