@@ -90,6 +90,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PD_INL_EXACT
 #define PD_INL_EXACT __noinline__  // the exact polytope-vs-box node test (rare unless PD_EXACT_LEAVES)
 #endif
+#ifndef PD_PK_CULL
+#define PD_PK_CULL 0  // node bound (1) on the plane-distance lower bound (keeps w_i - w_max > 0) vs the radius
+#endif
 #ifndef PD_FLAT_NODES
 #define PD_FLAT_NODES 1  // descent: node tests on all 32 lanes (child lane & 7) instead of a lane < 8 branch
 #endif
@@ -184,6 +187,7 @@ struct Cell {
     double px, py, pz, pw;  // site (world), weight
     float fpx, fpy, fpz, fpw;
     float flo[3], fhi[3];   // cell AABB, site-local, rounded outward
+    float glo[3], ghi[3];   // the same box grown to contain the site: min(flo, 0), max(fhi, 0) (node bound (2))
     float vmax;             // max_k max(|lo_k|, |hi_k|)
     float sc[3], srad;      // bounding sphere of the cell (SPHERE tiers): center (site-local), radius
     int nv, np, nq;
@@ -436,17 +440,30 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
     float dw = c.fpw - lo_w.w;
     float dwn = fminf(0.f, dw);
     float r2 = dir_r2(c, allow, iso);
-    float rd = sqrt_up(r2 * d2);
-    culled = d2 + dwn - 2.f * rd > 1e-5f * (d2 - dwn + 2.f * rd);
+    float pk = 0.f;
+    if (PD_PK_CULL && PK && !paper) {
+        // (1) with the plane-distance bound of the priority, which keeps a positive w_i - w_max (the paper's
+        // d/2 + min(0, dw)/(2d) drops it): no site of the node has a plane nearer than pk, and no point of the
+        // cell is farther than r in the node's octants -- cull iff pk > r
+        pk = plane_key(d2, dw);
+        const float r = sqrt_up(r2);
+        culled = pk - r > 1e-5f * (fabsf(pk) + r);
+    } else {
+        float rd = sqrt_up(r2 * d2);
+        culled = d2 + dwn - 2.f * rd > 1e-5f * (d2 - dwn + 2.f * rd);
+    }
     if (!paper) {
-        float h0 = fmaxf(fmaxf(c.flo[0] * a0, c.flo[0] * b0), fmaxf(c.fhi[0] * a0, c.fhi[0] * b0));
-        float h1 = fmaxf(fmaxf(c.flo[1] * a1, c.flo[1] * b1), fmaxf(c.fhi[1] * a1, c.fhi[1] * b1));
-        float h2 = fmaxf(fmaxf(c.flo[2] * a2, c.flo[2] * b2), fmaxf(c.fhi[2] * a2, c.fhi[2] * b2));
+        // max over y in the box grown to contain the site (glo <= 0 <= ghi) and D_k in [a_k, b_k] of y_k D_k:
+        // with glo <= 0, glo a >= glo b; with ghi >= 0, ghi b >= ghi a -- two products per axis, not four
+        float h0 = fmaxf(c.glo[0] * a0, c.ghi[0] * b0);
+        float h1 = fmaxf(c.glo[1] * a1, c.ghi[1] * b1);
+        float h2 = fmaxf(c.glo[2] * a2, c.ghi[2] * b2);
         float H = h0 + h1 + h2;
         float mag = c.vmax * (fmaxf(fabsf(a0), fabsf(b0)) + fmaxf(fabsf(a1), fabsf(b1)) + fmaxf(fabsf(a2), fabsf(b2)));
         culled |= d2 + dw - 2.f * H > 1e-5f * (d2 + fabsf(dw) + 2.f * mag);
     }
     if (PK && PD_PLANE_KEY == 3) return plane_key(d2, dw) - sqrtf(r2);  // the nearest plane's depth in the cell
+    if (PD_PK_CULL && PK && !paper) return pk;
     if (PK) return plane_key(d2, dw);
     return d2 + dwn - r2;
 }
@@ -585,7 +602,10 @@ __device__ __forceinline__ void finish_aabb(Cell& c, const Box6& b) {
     // writes land before any lane reads the new ones
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 3; ++k) { c.flo[k] = lo[k]; c.fhi[k] = hi[k]; }
+    for (int k = 0; k < 3; ++k) {
+        c.flo[k] = lo[k]; c.fhi[k] = hi[k];
+        c.glo[k] = fminf(lo[k], 0.f); c.ghi[k] = fmaxf(hi[k], 0.f);
+    }
     c.vmax = vm;
     __syncwarp();
 }
@@ -1619,7 +1639,10 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
     }
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 3; ++k) { c.flo[k] = flo[k]; c.fhi[k] = fhi[k]; }
+    for (int k = 0; k < 3; ++k) {
+        c.flo[k] = flo[k]; c.fhi[k] = fhi[k];
+        c.glo[k] = fminf(flo[k], 0.f); c.ghi[k] = fmaxf(fhi[k], 0.f);
+    }
     c.vmax = vm;
     __syncwarp();
 }
