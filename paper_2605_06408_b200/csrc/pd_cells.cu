@@ -91,7 +91,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #define PD_INL_EXACT __noinline__  // the exact polytope-vs-box node test (rare unless PD_EXACT_LEAVES)
 #endif
 #ifndef PD_PK_CULL
-#define PD_PK_CULL 0  // node bound (1) on the plane-distance lower bound (keeps w_i - w_max > 0) vs the radius
+#define PD_PK_CULL 1  // node bound (1) on the plane-distance lower bound (keeps w_i - w_max > 0) vs the radius
 #endif
 #ifndef PD_FLAT_NODES
 #define PD_FLAT_NODES 1  // descent: node tests on all 32 lanes (child lane & 7) instead of a lane < 8 branch
