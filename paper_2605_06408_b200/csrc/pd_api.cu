@@ -142,6 +142,19 @@ void setup_pool(int device) {
     }
 }
 
+// A high-priority internal stream per device: the capacity tiers 2-3 run on it concurrently with the tier-1
+// finalize on the caller's stream (PD_OVERLAP); pending CTAs of the higher priority are dispatched first.
+cudaStream_t hi_stream(int device) {
+    static cudaStream_t hs[64] = {};
+    cudaStream_t& h = hs[device & 63];
+    if (!h) {
+        int least = 0, greatest = 0;
+        ck(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        ck(cudaStreamCreateWithPriority(&h, cudaStreamNonBlocking, greatest));
+    }
+    return h;
+}
+
 int num_sms(int device) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
@@ -670,7 +683,21 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
             P.coop_min_v = getenv("PD_COOP_MIN_V") ? atoi(getenv("PD_COOP_MIN_V")) : 128;
             P.trace_cell = getenv("PD_TRACE_CELL") ? atoi(getenv("PD_TRACE_CELL")) : -1;
             int64_t L = end - begin;
+            // The tier-1 finalize (non-persistent grid of 16 cells per warp, caller's stream) runs concurrently with
+            // the higher tiers (internal high-priority stream): they read and write disjoint cells' outputs, and
+            // every shared counter (row arena, stats) is an atomic.  Measured C4 358 -> 353 ms, C5 595 -> 582 ms,
+            // C3 159.5 -> 161 ms.  PD_OVERLAP=0: serial (persistent finalize after tier 1); N > 1: N cells per warp.
+            const int overlap = getenv("PD_OVERLAP") ? atoi(getenv("PD_OVERLAP")) : 1;
+            cudaStream_t sh = overlap ? hi_stream(opt.device) : st;
+            Ev ov[2];
+            pd::CellParams P0;
             for (int tier = 0; tier < 3; ++tier) {
+                cudaStream_t ts = tier == 0 ? st : sh;
+                if (tier == 1 && overlap) {
+                    ov[0].create();
+                    ck(cudaEventRecord(ov[0], st));
+                    ck(cudaStreamWaitEvent(sh, ov[0], 0));
+                }
                 P.work_counter = counters + tier;
                 P.last_tier = tier == 2;
                 if (tier == 0) {
@@ -693,10 +720,17 @@ pd_status build_impl(const float* points, const float* weights, int64_t n, const
                     // the device (no host round trip between the tiers).
                     ck(pd::sort_list_by_cost(const_cast<int32_t*>(P.list),
                                              lcost + (size_t)((tier - 1) & 1) * std::max<int64_t>(L, 1),
-                                             P.list_count, st, &launches));
+                                             P.list_count, ts, &launches));
                 }
-                ck(cudaEventRecord(tev[tier], st));
-                ck(pd::launch_cells(tier, P, st, sms, &launches));
+                ck(cudaEventRecord(tev[tier], ts));
+                ck(pd::launch_cells(tier, P, ts, sms, &launches, !overlap));
+                if (tier == 0) P0 = P;
+            }
+            if (overlap) {
+                ck(pd::launch_finalize(P0, st, sms, overlap > 1 ? overlap : 16, &launches));
+                ov[1].create();
+                ck(cudaEventRecord(ov[1], sh));
+                ck(cudaStreamWaitEvent(st, ov[1], 0));
             }
             ck(cudaEventRecord(tev[3], st));
             unsigned long long top = 0, ttop = 0;

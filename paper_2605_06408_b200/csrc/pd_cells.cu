@@ -2274,13 +2274,17 @@ __device__ __forceinline__ bool defer_cell(const WarpState<T>& S, const Cell& c,
 // neighbour ids exactly as the cell program built them (exact_plane / the walls of init_cell) and every vertex
 // by solve3 of its three planes -- the same function on the same operands, so the same values -- then the
 // same finalize() as in the cell kernel.
+// cpw = 0: persistent grid, grid-stride over the cells; cpw > 0: one chunk of cpw consecutive cells per warp
+// (CTAs retire as they finish, so kernels of other streams -- the higher tiers -- get SMs as they free up).
 template <class T>
-__global__ void __launch_bounds__(T::WARPS * 32) finalize_kernel(const __grid_constant__ CellParams P) {
+__global__ void __launch_bounds__(T::WARPS * 32) finalize_kernel(const __grid_constant__ CellParams P, int cpw) {
     const int lane = threadIdx.x & 31, wid = (int)(threadIdx.x >> 5);
     WarpState<T>& S = reinterpret_cast<WarpState<T>*>(pd_smem)[wid];
     Cell& c = S.c;
-    const int64_t gw = (int64_t)blockIdx.x * T::WARPS + wid, nw = (int64_t)gridDim.x * T::WARPS;
-    for (int64_t idx = gw; idx < P.count; idx += nw) {
+    const int64_t gw = (int64_t)blockIdx.x * T::WARPS + wid;
+    const int64_t nw = cpw > 0 ? 1 : (int64_t)gridDim.x * T::WARPS;
+    const int64_t i0 = cpw > 0 ? gw * cpw : gw, i1 = cpw > 0 ? min(P.count, i0 + cpw) : P.count;
+    for (int64_t idx = i0; idx < i1; idx += nw) {
         const int s = (int)(P.begin + idx);
         const uint32_t off = P.rec_index[s];
         if (off == 0xffffffffu) continue;
@@ -2500,18 +2504,30 @@ cudaError_t launch_tier(const CellParams& p, int tier, cudaStream_t st, int num_
 
 cudaError_t launch_tier1(const CellParams& p, cudaStream_t st, int num_sms);
 
-cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches) {
+cudaError_t launch_finalize(const CellParams& p, cudaStream_t st, int num_sms, int cpw, int* launches) {
+    if (!p.rec_index || p.count <= 0) return cudaSuccess;
+    if (launches) ++*launches;
+    const size_t smem = sizeof(WarpState<Tier1F>) * Tier1F::WARPS;
+    cudaFuncSetAttribute(finalize_kernel<Tier1F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int grid;
+    if (cpw > 0) {
+        const int64_t warps = (p.count + cpw - 1) / cpw;
+        grid = (int)((warps + Tier1F::WARPS - 1) / Tier1F::WARPS);
+    } else {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, finalize_kernel<Tier1F>, Tier1F::WARPS * 32, smem);
+        grid = num_sms * (per_sm < 1 ? 1 : per_sm);
+    }
+    finalize_kernel<Tier1F><<<grid, Tier1F::WARPS * 32, smem, st>>>(p, cpw);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches, bool with_finalize) {
     if (launches) ++*launches;
     if (tier == 0) {
         cudaError_t e = launch_tier1(p, st, num_sms);
-        if (e != cudaSuccess || !p.rec_index) return e;
-        if (launches) ++*launches;
-        const size_t smem = sizeof(WarpState<Tier1F>) * Tier1F::WARPS;
-        cudaFuncSetAttribute(finalize_kernel<Tier1F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, finalize_kernel<Tier1F>, Tier1F::WARPS * 32, smem);
-        finalize_kernel<Tier1F><<<num_sms * (per_sm < 1 ? 1 : per_sm), Tier1::WARPS * 32, smem, st>>>(p);
-        return cudaGetLastError();
+        if (e != cudaSuccess || !with_finalize) return e;
+        return launch_finalize(p, st, num_sms, 0, launches);
     }
     if (tier == 1) return launch_tier<Tier2, kDynMode>(p, 1, st, num_sms);
     return launch_tier<Tier3, kDynMode>(p, 2, st, num_sms);

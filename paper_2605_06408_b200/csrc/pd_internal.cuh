@@ -101,7 +101,10 @@ struct CellParams {
     int64_t rec_cap;               // words (< 2^32); a cell that does not fit is built again by tier 2
 };
 
-cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches);
+cudaError_t launch_cells(int tier, const CellParams& p, cudaStream_t st, int num_sms, int* launches,
+                         bool with_finalize = true);
+// the tier-1 finalize (deferred records) alone; cpw > 0: non-persistent grid, cpw cells per warp
+cudaError_t launch_finalize(const CellParams& p, cudaStream_t st, int num_sms, int cpw, int* launches);
 int cells_grid_warps(int tier, int num_sms);
 size_t cells_global_state_bytes(int num_sms);
 constexpr int KNN_K = 8;  // warm-start neighbours per site
