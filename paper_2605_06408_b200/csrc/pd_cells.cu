@@ -93,6 +93,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PD_PK_CULL
 #define PD_PK_CULL 1  // node bound (1) on the plane-distance lower bound (keeps w_i - w_max > 0) vs the radius
 #endif
+#ifndef PD_PARK
+#define PD_PARK 0  // park the queue counts in shared memory across a leaf (lower register pressure)
+#endif
 #ifndef PD_FLAT_NODES
 #define PD_FLAT_NODES 1  // descent: node tests on all 32 lanes (child lane & 7) instead of a lane < 8 branch
 #endif
@@ -188,10 +191,12 @@ struct Cell {
     float fpx, fpy, fpz, fpw;
     float flo[3], fhi[3];   // cell AABB, site-local, rounded outward
     float glo[3], ghi[3];   // the same box grown to contain the site: min(flo, 0), max(fhi, 0) (node bound (2))
+    float flo2[3], fhi2[3]; // flo^2, fhi^2 (the directional radius of node bound (1))
     float vmax;             // max_k max(|lo_k|, |hi_k|)
     float sc[3], srad;      // bounding sphere of the cell (SPHERE tiers): center (site-local), radius
     int nv, np, nq;
     int degraded;           // a topology-consistency check failed (PD_CELL_DEGRADED)
+    int t_nq, t_ns;         // traversal state parked across a leaf (PD_PARK)
     int self;               // Morton index
     int self_orig;
 };
@@ -381,7 +386,7 @@ __device__ __forceinline__ float dir_r2(const Cell& c, unsigned allow, bool iso)
     float r2 = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        float h2 = c.fhi[k] * c.fhi[k], l2 = c.flo[k] * c.flo[k];
+        const float h2 = c.fhi2[k], l2 = c.flo2[k];
         float a = (iso || (allow & (1u << (2 * k)))) ? h2 : 0.f;
         float b = (iso || (allow & (2u << (2 * k)))) ? l2 : 0.f;
         r2 += fmaxf(a, b);
@@ -412,8 +417,11 @@ __device__ __forceinline__ float dir_r2(const Cell& c, unsigned allow, bool iso)
 #define PD_PLANE_KEY 2  // 0: Alg. 1's priority everywhere; 1: plane-distance bound in tiers 2-3; 2: in every tier
 #endif
 __device__ __forceinline__ float plane_key(float d2, float dw) {
-    if (dw > 0.f && d2 < dw) return dw * rsqrtf(dw);  // sqrt(dw): approximate is fine, it only orders
-    return d2 > 0.f ? 0.5f * (d2 + dw) * rsqrtf(d2) : -INFINITY;
+    // branch-free, one MUFU.RSQ: m = max(d2, dw) is d2 unless d2 < dw (then the bound is sqrt(dw) = dw / sqrt(dw));
+    // d2 = 0 with dw <= 0 gives a huge negative value (the bound is -inf there; 0 when dw = 0 too)
+    const float m = fmaxf(fmaxf(d2, dw), 1e-30f);
+    const float rs = rsqrtf(m);
+    return d2 < dw ? dw * rs : 0.5f * (d2 + dw) * rs;
 }
 template <bool PK = false>
 __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi_l, unsigned flags, bool& culled) {
@@ -446,7 +454,7 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
         // d/2 + min(0, dw)/(2d) drops it): no site of the node has a plane nearer than pk, and no point of the
         // cell is farther than r in the node's octants -- cull iff pk > r
         pk = plane_key(d2, dw);
-        const float r = sqrt_up(r2);
+        const float r = r2 > 0.f ? r2 * rsqrtf(r2) * (1.f + 1e-6f) : 0.f;  // within the 1e-5 margin
         culled = pk - r > 1e-5f * (fabsf(pk) + r);
     } else {
         float rd = sqrt_up(r2 * d2);
@@ -605,6 +613,7 @@ __device__ __forceinline__ void finish_aabb(Cell& c, const Box6& b) {
     for (int k = 0; k < 3; ++k) {
         c.flo[k] = lo[k]; c.fhi[k] = hi[k];
         c.glo[k] = fminf(lo[k], 0.f); c.ghi[k] = fmaxf(hi[k], 0.f);
+        c.flo2[k] = lo[k] * lo[k]; c.fhi2[k] = hi[k] * hi[k];
     }
     c.vmax = vm;
     __syncwarp();
@@ -1396,7 +1405,11 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                 __syncwarp();
                 PT_BEGIN(t_leaf);
                 const unsigned ncl0 = cnt.ncl;
+                // PD_PARK: warp-uniform traversal state parked in shared memory across the leaf (register
+                // pressure of the inlined clip), reloaded below
+                if (PD_PARK) { c.t_nq = nq; c.t_ns = ns; }
                 int st = process_leaf<T, MODE>(S, c, lane, node, warm, P, cnt);
+                if (PD_PARK) { nq = *(volatile int*)&c.t_nq; ns = *(volatile int*)&c.t_ns; }
                 PT_END(t_leaf, 2);
                 if (st != ST_OK) return st;
                 if (cnt.ncl != ncl0) dirty = true;
@@ -1642,6 +1655,7 @@ __device__ __noinline__ void init_cell(WarpState<T>& S, Cell& c, int lane, const
     for (int k = 0; k < 3; ++k) {
         c.flo[k] = flo[k]; c.fhi[k] = fhi[k];
         c.glo[k] = fminf(flo[k], 0.f); c.ghi[k] = fmaxf(fhi[k], 0.f);
+        c.flo2[k] = flo[k] * flo[k]; c.fhi2[k] = fhi[k] * fhi[k];
     }
     c.vmax = vm;
     __syncwarp();
