@@ -94,7 +94,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #define PD_PK_CULL 1  // node bound (1) on the plane-distance lower bound (keeps w_i - w_max > 0) vs the radius
 #endif
 #ifndef PD_PARK
-#define PD_PARK 0  // park the queue counts in shared memory across a leaf (lower register pressure)
+#define PD_PARK 1  // park the queue counts in shared memory across a leaf (lower register pressure)
 #endif
 #ifndef PD_FLAT_NODES
 #define PD_FLAT_NODES 1  // descent: node tests on all 32 lanes (child lane & 7) instead of a lane < 8 branch
@@ -140,7 +140,7 @@ struct TierCfg {
 };
 
 #ifndef PD_T1_MINB
-#define PD_T1_MINB 5  // resident CTAs per SM (register cap 96)
+#define PD_T1_MINB 6  // resident CTAs per SM (register cap 80; 5: 96 registers, measured 2.5% slower)
 #endif
 #ifndef PD_T1_WARPS
 #define PD_T1_WARPS 4  // 1: one-warp CTAs (constant smem address) measured 9% lower issue efficiency on C4
