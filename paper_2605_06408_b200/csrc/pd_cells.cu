@@ -93,6 +93,12 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PD_PK_CULL
 #define PD_PK_CULL 1  // node bound (1) on the plane-distance lower bound (keeps w_i - w_max > 0) vs the radius
 #endif
+#ifndef PD_KEY_SMEM
+#define PD_KEY_SMEM 0  // the leaf candidates' order keys in shared memory instead of a register held through clip()
+#endif
+#ifndef PD_FAST_RCP
+#define PD_FAST_RCP 1  // solve3: 1/det by a MUFU seed + 2 Newton steps instead of the IEEE FP64 division
+#endif
 #ifndef PD_PARK
 #define PD_PARK 1  // park the queue counts in shared memory across a leaf (lower register pressure)
 #endif
@@ -245,6 +251,7 @@ struct __align__(16) WarpState {
     uint16_t pmap[T::FIN ? 1 : T::PMAX];  // plane GC remap
     float4 cpl[T::FIN ? 1 : 32];  // a leaf's candidates, by rank: FP32 plane (D = p_j - p_i, dd = q/2)
     __align__(16) float cmg[T::FIN ? 4 : 32];  //   and its certification margin (kept in smem, not registers, through clip())
+    int ckey[(T::FIN || !PD_KEY_SMEM) ? 1 : 32];  // the candidates' order keys (PD_KEY_SMEM), by slot
     uint32_t ebits[T::EBW];       // hole-edge parity bitmap (zero between clips)
 };
 
@@ -717,7 +724,17 @@ __device__ __forceinline__ void solve3(const double4* pl, int ia, int ib, int ic
         const double abx = a.y * b.z - a.z * b.y, aby = a.z * b.x - a.x * b.z, abz = a.x * b.y - a.y * b.x;
         x += c.w * abx; y += c.w * aby; z += c.w * abz;
     }
-    const double inv = 1.0 / det;
+    double inv;
+    if (PD_FAST_RCP) {
+        // MUFU reciprocal seed + two Newton steps (quadratic convergence: full FP64 precision, within 1 ulp of
+        // 1/det) instead of the IEEE division sequence; the same function builds every vertex everywhere
+        // (clip, certification, finalize_kernel), so all FP64 positions stay consistent
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(det));
+        inv = fma(inv, fma(-det, inv, 1.0), inv);
+        inv = fma(inv, fma(-det, inv, 1.0), inv);
+    } else {
+        inv = 1.0 / det;
+    }
     x *= inv; y *= inv; z *= inv;
 }
 
@@ -1137,7 +1154,11 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
     const unsigned mask0 = mask;
     const int ncand = __popc(mask0);
     const int myslot = PD_PRETEST_COMPACT ? __popc(mask0 & lanemask_lt()) : lane;
-    if (cand) { S.cpl[myslot] = make_float4(Dx, Dy, Dz, dd); S.cmg[myslot] = m; }
+    if (cand) {
+        S.cpl[myslot] = make_float4(Dx, Dy, Dz, dd);
+        S.cmg[myslot] = m;
+        if (PD_KEY_SMEM) S.ckey[myslot] = ford(key);
+    }
     if (PD_PRETEST_COMPACT && lane >= ncand && lane < ((ncand + 3) & ~3)) {  // the last group's padding
         S.cpl[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
         S.cmg[lane] = 0.f;
@@ -1196,8 +1217,9 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
     }
     int nclip = 0;
     while (mask) {
-        int kmin = __reduce_min_sync(FULL, cand ? ford(key) : 0x7fffffff);
-        unsigned lead = __ballot_sync(FULL, cand && ford(key) == kmin);
+        const int kk = !cand ? 0x7fffffff : (PD_KEY_SMEM ? S.ckey[myslot] : ford(key));  // smem: not live across clip
+        int kmin = __reduce_min_sync(FULL, kk);
+        unsigned lead = __ballot_sync(FULL, cand && kk == kmin);
         int src = __ffs(lead) - 1;
         if (lane == src) cand = false;
         // Fast reject, lane = vertex: the plane (D, dd) of the leaf's candidate pass, its margin m (from the
