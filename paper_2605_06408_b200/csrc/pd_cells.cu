@@ -45,6 +45,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #define PD_ASSERT(c) (void)0
 #endif
 
+#ifndef PD_LAZY_POP_TOP
+#define PD_LAZY_POP_TOP 1  // cooperative top tier: lazy pop (its queue is long; the plane-distance keys never go stale)
+#endif
 #ifndef PD_LAZY_POP
 #define PD_LAZY_POP 0
 #endif
@@ -219,7 +222,7 @@ struct __align__(16) WarpState {
         struct {                  // traversal: priority queue of pushed child records
             float4 qlo[T::QMAX];  // (lo, maxw)
             float4 qhi[T::QMAX];  // (hi, link)
-            float qkey[(PD_LAZY_POP || PD_CLEAN_POP) ? T::QMAX : 1];  // priority (lazy / clean pop)
+            float qkey[(PD_LAZY_POP || PD_CLEAN_POP || (PD_LAZY_POP_TOP && T::COOP)) ? T::QMAX : 1];  // priority
         };
         struct {                  // finalize (the queue is dead by then)
             union {
@@ -484,6 +487,11 @@ __device__ __forceinline__ float node_test(const Cell& c, float4 lo_w, float4 hi
 }
 template <class T>
 constexpr bool kCleanPop = PD_CLEAN_POP && !PD_LAZY_POP && !T::COOP;
+// Lazy pop (the paper's): pop the least key, test only that entry.  With the plane-distance keys (which
+// do not depend on the cell) the order is exact; dead entries are found one at a time when they reach the top.
+// Measured slower in tier 1 (short queues, many dead entries), used in the cooperative top tier (long queues).
+template <class T>
+constexpr bool kLazyPop = PD_LAZY_POP || (PD_LAZY_POP_TOP && T::COOP && (PD_PLANE_KEY >= 1));
 template <class T>
 constexpr bool kPlaneKey = PD_PLANE_KEY >= 2 || (PD_PLANE_KEY == 1 && T::SPHERE);
 
@@ -1398,7 +1406,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     if (ns + tos > spill_cap) return ST_OVERFLOW;
                     if (push) {
                         if (rank < room) {
-                            if (PD_LAZY_POP || kCleanPop<T>) S.qkey[nq + rank] = key;
+                            if (kLazyPop<T> || kCleanPop<T>) S.qkey[nq + rank] = key;
                             PD_ASSERT(nq + rank < T::QMAX);
                             qlo[nq + rank] = lo_w;
                             qhi[nq + rank] = hi_l;
@@ -1451,7 +1459,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             int mm = min(ns, T::QMAX);
             for (int t = lane; t < mm; t += 32) {
                 NodeChild e = spill[ns - mm + t];
-                if (PD_LAZY_POP) {
+                if (kLazyPop<T>) {
                     bool cu;
                     S.qkey[t] = node_test<kPlaneKey<T>>(c, e.lo_w, e.hi_l, flags, cu);
                 }
@@ -1481,7 +1489,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             have = true;
             continue;
         }
-        if (PD_LAZY_POP) {
+        if (kLazyPop<T>) {
             // the paper's unsorted-queue pop: min over the push-time priorities,
             // re-validate only the popped entry (Alg. 1 lines 25-29), fill its hole with the last one
             int bk = 0x7fffffff, bs = -1;
