@@ -178,7 +178,10 @@ using Tier1F = TierCfg<PD_T1_V, PD_T1_P, PD_T1_Q, PD_T1_WARPS, PD_T1_MINB, false
 #ifndef PD_T2_COOP
 #define PD_T2_COOP 0  // measured slower on C3/C4 (the heavy tier-2 cells are traversal-bound), kept as an option
 #endif
-using Tier2 = TierCfg<384, 192, 256, 4, PD_T2_COOP ? 4 : 1, false, PD_T2_COOP != 0, true>;
+#ifndef PD_T2_WARPS
+#define PD_T2_WARPS 6  // warps (cells) per tier-2 CTA, one CTA per SM (35.6 KB of shared memory per warp; 4: C3 +7%)
+#endif
+using Tier2 = TierCfg<384, 192, 256, PD_T2_WARPS, PD_T2_COOP ? 4 : 1, false, PD_T2_COOP != 0, true>;
 // Top tier: state in global memory (L1/L2-cached), 64-bit plane-index triplets; for the rare cells
 // with thousands of faces (heavy-tailed weights, SURVEY.md §7 hard part 3).
 // One cell per CTA: its 16 warps share every O(V) pass (classification, exact node tests, AABB,
