@@ -64,7 +64,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #define PD_LAZY_COMPACT 0  // swap-remove the popped queue entry while >= 3/4 are alive (all tiers)
 #endif
 #ifndef PD_LEAF_AABB
-#define PD_LEAF_AABB 0  // tier 1: the cell AABB refreshed once per leaf (after its clips), not after every clip
+#define PD_LEAF_AABB 1  // tier 1: the cell AABB refreshed once per leaf (after its clips), not after every clip (C4 -3%)
 #endif
 #ifndef PD_FUSED_AABB
 #define PD_FUSED_AABB 1  // tier 1: the new AABB from the classification pass (measured 3.5% faster on C4)
