@@ -96,6 +96,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PD_PK_CULL
 #define PD_PK_CULL 1  // node bound (1) on the plane-distance lower bound (keeps w_i - w_max > 0) vs the radius
 #endif
+#ifndef PD_FIN_BATCH
+#define PD_FIN_BATCH 0  // finalize_kernel (chunked): per-chunk batched loads of the record headers / sites / ids (no gain measured)
+#endif
 #ifndef PD_KEY_SMEM
 #define PD_KEY_SMEM 0  // the leaf candidates' order keys in shared memory instead of a register held through clip()
 #endif
@@ -2331,24 +2334,50 @@ __global__ void __launch_bounds__(T::WARPS * 32) finalize_kernel(const __grid_co
     const int64_t gw = (int64_t)blockIdx.x * T::WARPS + wid;
     const int64_t nw = cpw > 0 ? 1 : (int64_t)gridDim.x * T::WARPS;
     const int64_t i0 = cpw > 0 ? gw * cpw : gw, i1 = cpw > 0 ? min(P.count, i0 + cpw) : P.count;
+    // chunked mode (cpw <= 32): the chunk's record offsets, headers, degraded words, sites and original ids are
+    // loaded once, lane = cell, and handed out by shuffles (one round of global latency per chunk, not per cell)
+    const bool batch = PD_FIN_BATCH && cpw > 0 && cpw <= 32;
+    uint32_t b_off = 0xffffffffu, b_h0 = 0u, b_deg = 0u;
+    int b_orig = 0;
+    float4 b_site = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (batch && i0 + lane < i1) {
+        const int sl = (int)(P.begin + i0 + lane);
+        b_off = P.rec_index[sl];
+        b_site = __ldg(&P.sites[sl]);
+        b_orig = __ldg(&P.perm[sl]);
+        if (b_off != 0xffffffffu) { b_h0 = P.rec_arena[b_off]; b_deg = P.rec_arena[b_off + 1]; }
+    }
     for (int64_t idx = i0; idx < i1; idx += nw) {
         const int s = (int)(P.begin + idx);
-        const uint32_t off = P.rec_index[s];
+        const int k = (int)(idx - i0);
+        const uint32_t off = batch ? __shfl_sync(FULL, b_off, k) : P.rec_index[s];
         if (off == 0xffffffffu) continue;
         const uint32_t* rec = P.rec_arena + off;
-        const uint32_t h0 = rec[0];
+        const uint32_t h0 = batch ? __shfl_sync(FULL, b_h0, k) : rec[0];
         const int nv = (int)(h0 & 0xffffu), np = (int)(h0 >> 16);
         PD_ASSERT(nv >= 4 && nv <= T::VMAX && np >= 4 && np <= T::PMAX && off + 2u + (uint32_t)(nv + np) <= P.rec_cap);
-        const float4 site = __ldg(&P.sites[s]);
+        float4 site;
+        int orig;
+        uint32_t deg;
+        if (batch) {
+            site.x = __shfl_sync(FULL, b_site.x, k); site.y = __shfl_sync(FULL, b_site.y, k);
+            site.z = __shfl_sync(FULL, b_site.z, k); site.w = __shfl_sync(FULL, b_site.w, k);
+            orig = __shfl_sync(FULL, b_orig, k);
+            deg = __shfl_sync(FULL, b_deg, k);
+        } else {
+            site = __ldg(&P.sites[s]);
+            orig = __ldg(&P.perm[s]);
+            deg = rec[1];
+        }
         __syncwarp();
         if (lane == 0) {
             c.fpx = site.x; c.fpy = site.y; c.fpz = site.z; c.fpw = site.w;
             c.px = site.x; c.py = site.y; c.pz = site.z; c.pw = site.w;
             c.self = s;
-            c.self_orig = __ldg(&P.perm[s]);
+            c.self_orig = orig;
             c.nv = nv;
             c.np = np;
-            c.degraded = (int)rec[1];
+            c.degraded = (int)deg;
         }
         __syncwarp();
         for (int f = lane; f < np; f += 32) {
