@@ -1274,7 +1274,8 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
             if (kStats<MODE>) cnt.clips++;
             cnt.ncl++;
             cnt.work += 8;
-            if (cand && site_culled_pl<T::SPHERE>(c, S.cpl[myslot], flags)) cand = false;
+            // (with the per-leaf AABB the box has not changed since the leaf's site cull: nothing new to cull)
+            if (!kLeafAabb<T> && cand && site_culled_pl<T::SPHERE>(c, S.cpl[myslot], flags)) cand = false;
             if (PD_REFILTER && PD_PRETEST_COMPACT && !batched) {
                 if (__popc(__ballot_sync(FULL, cand)) >= PD_REFILTER_MIN) {
                     const unsigned hr = pretest(__reduce_or_sync(FULL, cand ? 1u << myslot : 0u));
