@@ -251,7 +251,8 @@ pd_status pd_sort_pairs_u64(const uint64_t* keys_in, const uint32_t* vals_in, in
                             uint32_t* vals_out, void* stream);
 
 /* Release the per-device build workspace (temporaries are cached across builds in persistent device
- * chunks, DESIGN.md §6 "Memory") and the cached pinned host buffers of freed PD_OUT_HOST results.
+ * chunks, DESIGN.md §6 "Memory"), the internal high-priority stream the capacity tiers 2-3 run on, and
+ * the cached pinned host buffers of freed PD_OUT_HOST results.
  * Waits for a build in flight on `device`; results stay valid.  Errors: PD_EINVAL (device out of
  * range), PD_ECUDA. */
 pd_status pd_trim(int device);

@@ -144,9 +144,12 @@ void setup_pool(int device) {
 
 // A high-priority internal stream per device: the capacity tiers 2-3 run on it concurrently with the tier-1
 // finalize on the caller's stream (PD_OVERLAP); pending CTAs of the higher priority are dispatched first.
-cudaStream_t hi_stream(int device) {
+cudaStream_t& hi_stream_slot(int device) {
     static cudaStream_t hs[64] = {};
-    cudaStream_t& h = hs[device & 63];
+    return hs[device & 63];
+}
+cudaStream_t hi_stream(int device) {
+    cudaStream_t& h = hi_stream_slot(device);
     if (!h) {
         int least = 0, greatest = 0;
         ck(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -1072,6 +1075,10 @@ pd_status pd_trim(int device) {
     for (auto& c : W.chunks) cudaFree(c.first);
     W.chunks.clear();
     W.reset();
+    if (cudaStream_t& h = hi_stream_slot(device)) {  // the internal stream of the higher tiers
+        cudaStreamDestroy(h);
+        h = nullptr;
+    }
     pinned().trim();
     cudaSetDevice(cur);
     return PD_OK;
