@@ -280,6 +280,17 @@ def test_determinism_bitwise():
         assert np.array_equal(getattr(a, k), getattr(b, k)), k
 
 
+def test_trim_then_rebuild_identical():
+    """pd_trim releases the cached workspace and the internal stream of the higher tiers; the next build
+    re-creates them and returns the same diagram bit for bit (tiers 2-3 launch on that stream every build)."""
+    wl = pdgen.make("C3", n=20011)
+    a = _gpu(wl, flags=pd.STATS)
+    pd.trim(0)
+    b = _gpu(wl, flags=pd.STATS)
+    for k in ("offsets", "neighbors", "areas", "volumes", "surface", "flags"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
 def test_host_and_device_inputs_identical():
     wl = pdgen.make("C3", n=7001)
     a = _gpu(wl)
