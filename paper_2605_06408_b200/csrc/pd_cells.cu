@@ -120,6 +120,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PD_REFILTER_MIN
 #define PD_REFILTER_MIN 2  // ... when at least this many remain
 #endif
+#ifndef PD_PRETEST_MIN
+#define PD_PRETEST_MIN 1  // pre-test a leaf's candidates only when at least this many survive the site cull (2: 8% slower)
+#endif
 #ifndef PD_PRETEST_COMPACT
 #define PD_PRETEST_COMPACT 1  // the pre-test's candidate planes packed by rank (no empty groups of 4)
 #endif
@@ -1204,7 +1207,7 @@ __device__ PD_INL_LEAF int process_cands(WarpState<T>& S, Cell& c, int lane, int
         }
         return __reduce_or_sync(FULL, hit);
     };
-    if (PD_PRETEST && PD_PRETEST_COMPACT && !batched) {
+    if (PD_PRETEST && PD_PRETEST_COMPACT && !batched && ncand >= PD_PRETEST_MIN) {
         const unsigned hr = pretest(ncand == 32 ? FULL : (1u << ncand) - 1u);
         cand = cand && ((hr >> myslot) & 1u);
         mask = __ballot_sync(FULL, cand);
