@@ -100,7 +100,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #define PD_FIN_BATCH 0  // finalize_kernel (chunked): per-chunk batched loads of the record headers / sites / ids (no gain measured)
 #endif
 #ifndef PD_KEY_SMEM
-#define PD_KEY_SMEM 0  // the leaf candidates' order keys in shared memory instead of a register held through clip()
+#define PD_KEY_SMEM 1  // the leaf candidates' order keys in shared memory instead of a register held through clip()
 #endif
 #ifndef PD_FAST_RCP
 #define PD_FAST_RCP 1  // solve3: 1/det by a MUFU seed + 2 Newton steps instead of the IEEE FP64 division
@@ -120,6 +120,10 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PD_REFILTER_MIN
 #define PD_REFILTER_MIN 2  // ... when at least this many remain
 #endif
+#ifndef PD_VISITS_BY_WORK
+#define PD_VISITS_BY_WORK 1  // exact node tests switch on by the work counter (work/16) instead of a visit counter
+#endif
+#define PD_VISITS(cnt) (PD_VISITS_BY_WORK ? (unsigned long long)((cnt).work >> 4) : (unsigned long long)(cnt).visited)
 #ifndef PD_PRETEST_MIN
 #define PD_PRETEST_MIN 1  // pre-test a leaf's candidates only when at least this many survive the site cull (2: 8% slower)
 #endif
@@ -155,7 +159,7 @@ struct TierCfg {
 };
 
 #ifndef PD_T1_MINB
-#define PD_T1_MINB 6  // resident CTAs per SM (register cap 80; 5: 96 registers, measured 2.5% slower)
+#define PD_T1_MINB 7  // resident CTAs per SM (register cap 72, with the candidate keys in shared memory and no visit counter; 6: 80 registers, 0.5% slower on C4, 1.2% on C3; 5: 96 registers, 3% slower)
 #endif
 #ifndef PD_T1_WARPS
 #define PD_T1_WARPS 4  // 1: one-warp CTAs (constant smem address) measured 9% lower issue efficiency on C4
@@ -1353,7 +1357,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             while (node >= 0 && !warm) {  // descend (Alg. 1 lines 4-18), 8 children per visit
                 if (kStats<MODE>) cnt.nodes++;
                 cnt.work++;
-                cnt.visited++;
+                if (!PD_VISITS_BY_WORK) cnt.visited++;
                 float key = INFINITY;
                 bool culled = true;
                 float4 lo_w = make_float4(0, 0, 0, 0), hi_l = make_float4(0, 0, 0, 0);
@@ -1369,7 +1373,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
                     if (__float_as_int(hi_l.w) != EMPTY_LINK) key = node_test<kPlaneKey<T>>(c, lo_w, hi_l, flags, culled);
                 }
                 unsigned surv = __ballot_sync(FULL, !culled);
-                const bool ex_all = exact_on(flags, cnt.visited, P.exact_after);
+                const bool ex_all = exact_on(flags, PD_VISITS(cnt), P.exact_after);
                 // exact test on every surviving LEAF child (a leaf costs far more than the test), and on
                 // internal children too once the cell is heavy
                 const unsigned leafm = __ballot_sync(FULL, lane < WIDE && __float_as_int(hi_l.w) < 0);
@@ -1520,7 +1524,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             __syncwarp();
             bool culled;
             node_test<kPlaneKey<T>>(c, lo, hi, flags, culled);
-            if (!culled && (exact_on(flags, cnt.visited, P.exact_after) ||
+            if (!culled && (exact_on(flags, PD_VISITS(cnt), P.exact_after) ||
                             (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) && __float_as_int(hi.w) < 0)))
                 culled = node_exact_culled(S, c, lane, lo, hi);
             node = __float_as_int(hi.w);
@@ -1539,7 +1543,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
             const int gk = __reduce_min_sync(FULL, bk);
             const int bslot = __reduce_min_sync(FULL, bk == gk ? bs : 0x7fffffff);
             node = __float_as_int(qhi[bslot].w);
-            const bool popped_dead = (exact_on(flags, cnt.visited, P.exact_after) ||
+            const bool popped_dead = (exact_on(flags, PD_VISITS(cnt), P.exact_after) ||
                                       (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) && node < 0)) &&
                                      node_exact_culled(S, c, lane, qlo[bslot], qhi[bslot]);
             __syncwarp();
@@ -1600,7 +1604,7 @@ __device__ int traverse(WarpState<T>& S, Cell& c, int lane, const CellParams& P,
         unsigned lead = __ballot_sync(FULL, bestk == gk);
         int bslot = __shfl_sync(FULL, bests, __ffs(lead) - 1);
         node = __float_as_int(qhi[bslot].w);
-        bool popped_dead = (exact_on(flags, cnt.visited, P.exact_after) ||
+        bool popped_dead = (exact_on(flags, PD_VISITS(cnt), P.exact_after) ||
                             (PD_EXACT_LEAVES && !(flags & PD_NO_EXACT) && node < 0)) &&
                            node_exact_culled(S, c, lane, qlo[bslot], qhi[bslot]);
         if (PD_LAZY_COMPACT && alive_total < 0) {  // warp path: alive count from the chunk ballots
